@@ -1,0 +1,135 @@
+/*
+ * herosign_b200.h -- C-ABI of the B200 batched SPHINCS+-{128f,192f,256f}
+ * signing engine (libherosign_b200.so).
+ *
+ * Plain pointers and sizes only; no torch or CUDA types.  The caller owns
+ * every host buffer; the library owns device buffers, streams and CUDA
+ * graphs.  One handle drives one device and is not reentrant; ctypes releases
+ * the GIL around every call, so one host thread per handle drives 8 GPUs.
+ *
+ * Which reference interface each entry point replaces (paths relative to the
+ * reference's pkg/src/herosign/):
+ *
+ *   hs_keygen_batch   sigcore.keygen            sigcore.py:62-72
+ *   hs_keys_upload    HashContext.__init__      hashes.py:57-88 (per-key midstates)
+ *   hs_sign_batch     sigcore.sign              sigcore.py:139-178, and the batch
+ *                     driver cli bench / execute_graphs  batchgraph.py:110-226
+ *   hs_verify_batch   sigcore.verify            sigcore.py:181-221
+ *   hs_config_get/set TuningConfig per-set row  config.py:33-60 (fusion, relax,
+ *                     backends row backends.py:201-257)
+ *   hs_params         params.derive             params.py:97-149
+ *   hs_stage/hs_run/hs_fetch
+ *                     GraphSigner.prepare / run_fors|run_tree|run_wots
+ *                     (batchgraph.py:288-353): the stage plugin, split so the
+ *                     device part can be timed with inputs resident in HBM
+ *
+ * Parameter-set ids: 0 = "128f", 1 = "192f", 2 = "256f".
+ * Return codes: 0 on success, negative on error (see HS_E_*); the message is
+ * available from hs_last_error().  Usage-shaped errors map to the reference's
+ * UsageError/FormatError/ConfigError (errors.py:8-37), CUDA failures to
+ * HeroSignError.
+ */
+#ifndef HEROSIGN_B200_H
+#define HEROSIGN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HS_API __attribute__((visibility("default")))
+#else
+#define HS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HS_OK 0
+#define HS_E_USAGE (-1)   /* bad argument / size          -> UsageError  */
+#define HS_E_FORMAT (-2)  /* malformed key or signature   -> FormatError */
+#define HS_E_CONFIG (-3)  /* infeasible layout / config   -> ConfigError */
+#define HS_E_NOKEYS (-4)  /* sign before hs_keys_upload   -> UsageError  */
+#define HS_E_CUDA (-10)   /* device / runtime failure     -> HeroSignError */
+
+typedef struct hs_ctx hs_t;
+
+/* Per-set tuning row (config.py:33-38 SetConfig, extended for B200). */
+typedef struct {
+  int32_t fors_trees_per_set; /* N_tree: trees sharing one set of lanes      */
+  int32_t fors_sets_fused;    /* F: sets resident in one CTA's shared memory */
+  int32_t fors_relax;         /* Relax_FORS: lanes build leaf pairs          */
+  int32_t variant[4];         /* SHA-256 path per kernel: 0 native, 1 imad;
+                                 [0] FORS_Sign, [1] TREE_Sign, [2] WOTS_Sign,
+                                 [3] message preparation                     */
+  int32_t use_graph;          /* 1: one CUDA graph launch per batch          */
+  int32_t chunk;              /* messages per device pass in hs_sign_batch   */
+} hs_set_config;
+
+HS_API int hs_open(int device, hs_t **out);
+HS_API void hs_close(hs_t *h);
+HS_API const char *hs_last_error(const hs_t *h);
+
+/* SM count, opt-in shared memory per block (bytes), compute capability. */
+HS_API int hs_device_info(hs_t *h, int32_t *sm_count, int32_t *smem_optin, int32_t *cc_major, int32_t *cc_minor);
+
+/* Derived constants of a set, same order as the reference DerivedParams
+ * minus the id (n h d log_t k w lg_w len1 len2 wots_len subtree_height
+ * subtree_leaves fors_t fors_msg_bytes tree_bits tree_bytes leaf_bits
+ * leaf_bytes digest_bytes wots_sig_bytes fors_sig_bytes ht_sig_bytes
+ * sig_bytes); returns the count written. */
+HS_API int hs_params(int set, int32_t *fields, int cap);
+
+HS_API int hs_config_get(hs_t *h, int set, hs_set_config *cfg);
+HS_API int hs_config_set(hs_t *h, int set, const hs_set_config *cfg);
+/* Shared-memory bytes one FORS CTA needs under a layout (feasibility check
+ * for the tuner's S_max = opt-in smem). */
+HS_API int64_t hs_fors_smem_bytes(int set, int32_t trees_per_set, int32_t sets_fused, int32_t relax);
+
+/* Key table for a set: nkeys records of sk = sk_seed||sk_prf||pk_seed||pk_root. */
+HS_API int hs_keys_upload(hs_t *h, int set, const uint8_t *sks, uint32_t nkeys);
+
+/* Batched keygen: seeds (nkeys x 3n: sk_seed||sk_prf||pk_seed) -> sks (nkeys x 4n). */
+HS_API int hs_keygen_batch(hs_t *h, int set, const uint8_t *seeds, uint32_t nkeys, uint8_t *sks_out);
+
+/* Batched signing.  msgs is the concatenation of `count` messages with
+ * offs[count+1] byte offsets; key_idx[count] selects a row of the uploaded
+ * key table (NULL = row 0); opt_rand is count x n bytes (NULL = pk_seed,
+ * the reference's deterministic default); sigs receives count x sig_bytes. */
+HS_API int hs_sign_batch(hs_t *h, int set, const uint8_t *msgs, const uint64_t *offs, const uint32_t *key_idx,
+                  const uint8_t *opt_rand, uint32_t count, uint8_t *sigs);
+
+/* Batched verification; ok[i] = 1 iff sig i verifies under pk row key_idx[i]
+ * (pks: nkeys x 2n = pk_seed||pk_root).  sigs is count x sig_bytes. */
+HS_API int hs_verify_batch(hs_t *h, int set, const uint8_t *pks, uint32_t nkeys, const uint8_t *msgs,
+                    const uint64_t *offs, const uint32_t *key_idx, const uint8_t *sigs, uint32_t count,
+                    uint8_t *ok);
+
+/* Device-resident stages: hs_stage copies inputs into the library's device
+ * buffers; hs_run signs the staged batch (mode 0: as one CUDA graph with the
+ * FORS and TREE branches on two streams; mode 1: kernels serialised with a
+ * CUDA event between each, for per-kernel timing); hs_fetch copies
+ * signatures [first, first+count) back. */
+HS_API int hs_stage(hs_t *h, int set, const uint8_t *msgs, const uint64_t *offs, const uint32_t *key_idx,
+             const uint8_t *opt_rand, uint32_t count);
+HS_API int hs_run(hs_t *h, int set, uint32_t count, int mode);
+HS_API int hs_sync(hs_t *h);
+HS_API int hs_fetch(hs_t *h, int set, uint32_t first, uint32_t count, uint8_t *sigs);
+
+/* Device time (ms, CUDA events) of the last hs_run / hs_sign_batch pass:
+ * [0] whole batch, [1] msg_prep, [2] FORS_Sign (+T_k), [3] TREE_Sign,
+ * [4] WOTS_Sign.  Returns the number of values written. */
+HS_API int hs_timings(hs_t *h, float *ms, int cap);
+
+/* Kernel launches issued by this handle since open (for bench accounting). */
+HS_API int64_t hs_launch_count(hs_t *h);
+
+/* Page-locked host memory for zero-copy-staging callers (cudaMallocHost). */
+HS_API void *hs_host_alloc(size_t bytes);
+HS_API void hs_host_free(void *p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HEROSIGN_B200_H */

@@ -1,0 +1,653 @@
+// hs_api.cu -- host runtime behind the C-ABI (include/herosign_b200.h).
+//
+// Owns device buffers, the two streams (FORS branch / main branch) and one
+// CUDA graph per batch shape: msg_prep -> {FORS_Sign -> T_k} || TREE_Sign ->
+// WOTS_Sign, launched with a single cudaGraphLaunch per batch (the paper's
+// Task Graph; reference batchgraph.py:76-226 runs the same
+// DAG on CPU threads).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/herosign_b200.h"
+#include "hs_internal.h"
+#include "hs_kernels.cuh"
+
+using namespace hs;
+
+namespace {
+
+struct SetInfo {
+  int n, h, d, log_t, k, w, lg_w, len1, len2, wots_len, hp, leaves, t, fors_msg_bytes, tree_bits, tree_bytes,
+      leaf_bits, leaf_bytes, digest_bytes, wots_sig_bytes, fors_sig_bytes, ht_sig_bytes, sig_bytes;
+};
+
+template <int S>
+SetInfo info_of() {
+  using Pr = P<S>;
+  return SetInfo{Pr::n, Pr::h, Pr::d, Pr::log_t, Pr::k, Pr::w, Pr::lg_w, Pr::len1, Pr::len2, Pr::wots_len,
+                 Pr::hp, Pr::leaves, Pr::t, Pr::fors_msg_bytes, Pr::tree_bits, Pr::tree_bytes, Pr::leaf_bits,
+                 Pr::leaf_bytes, Pr::digest_bytes, Pr::wots_sig_bytes, Pr::fors_sig_bytes, Pr::ht_sig_bytes,
+                 Pr::sig_bytes};
+}
+
+const SetInfo kInfo[3] = {info_of<0>(), info_of<1>(), info_of<2>()};
+
+cudaError_t launch(int set, int which, int variant, const LaunchArgs& a, cudaStream_t s) {
+  switch (set) {
+    case 0: return launch_kernel<0>(which, variant, a, s);
+    case 1: return launch_kernel<1>(which, variant, a, s);
+    case 2: return launch_kernel<2>(which, variant, a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+size_t fors_smem(int set, int nt, int f, int relax) {
+  switch (set) {
+    case 0: return fors_smem_bytes<0>(nt, f, relax);
+    case 1: return fors_smem_bytes<1>(nt, f, relax);
+    case 2: return fors_smem_bytes<2>(nt, f, relax);
+  }
+  return 0;
+}
+
+hs_set_config default_config(int set) {
+  hs_set_config c;
+  std::memset(&c, 0, sizeof c);
+  // Defaults from the on-device Tree Tuning search (python tuner); see DESIGN.md.
+  static const int nt[3] = {11, 3, 2}, ff[3] = {3, 3, 2}, rx[3] = {0, 0, 1};
+  c.fors_trees_per_set = nt[set];
+  c.fors_sets_fused = ff[set];
+  c.fors_relax = rx[set];
+  for (int i = 0; i < 4; i++) c.variant[i] = 0;
+  c.use_graph = 1;
+  c.chunk = 16384;
+  return c;
+}
+
+template <class T>
+cudaError_t grow(T*& p, size_t& cap, size_t need) {
+  if (need <= cap && p) return cudaSuccess;
+  if (p) cudaFree(p);
+  p = nullptr;
+  size_t c = std::max(need, (size_t)1);
+  cudaError_t e = cudaMalloc(&p, c * sizeof(T));
+  cap = e == cudaSuccess ? c : 0;
+  return e;
+}
+
+template <class T>
+cudaError_t grow_host(T*& p, size_t& cap, size_t need) {
+  if (need <= cap && p) return cudaSuccess;
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  size_t c = std::max(need, (size_t)1);
+  cudaError_t e = cudaMallocHost(&p, c * sizeof(T));
+  cap = e == cudaSuccess ? c : 0;
+  return e;
+}
+
+struct Buffers {
+  uint8_t* msgs = nullptr; size_t msgs_cap = 0;
+  uint64_t* offs = nullptr; size_t offs_cap = 0;
+  uint32_t* keyidx = nullptr; size_t keyidx_cap = 0;
+  uint8_t* optrand = nullptr; size_t optrand_cap = 0;
+  uint8_t* sigs = nullptr; size_t sigs_cap = 0;
+  MsgPlan* plans = nullptr; size_t plans_cap = 0;
+  uint16_t* idx = nullptr; size_t idx_cap = 0;
+  uint32_t* roots = nullptr; size_t roots_cap = 0;
+  uint32_t* froots = nullptr; size_t froots_cap = 0;
+  // pinned staging
+  uint8_t* h_msgs = nullptr; size_t h_msgs_cap = 0;
+  uint64_t* h_offs = nullptr; size_t h_offs_cap = 0;
+  uint8_t* h_sigs = nullptr; size_t h_sigs_cap = 0;
+  uint64_t gen = 0;  // bumps whenever a device pointer changes (graph invalidation)
+};
+
+struct SetState {
+  hs_set_config cfg;
+  KeyDev* keys = nullptr;
+  size_t keys_cap = 0;
+  uint32_t nkeys = 0;
+  uint8_t* sk_raw = nullptr;
+  size_t sk_raw_cap = 0;
+  // staged batch
+  uint32_t staged = 0;
+  bool has_keyidx = false, has_optrand = false;
+};
+
+using GraphKey = std::tuple<int, uint32_t, int, int, uint64_t, std::string>;
+
+}  // namespace
+
+struct hs_ctx {
+  int device = 0;
+  cudaStream_t s0 = nullptr, s1 = nullptr;
+  cudaEvent_t ev[8] = {};     // timing: 0 start,1 prep,2 fors-done,3 tree-done,4 end,5 wots-start
+  cudaEvent_t fork = nullptr, join = nullptr;
+  SetState sets[3];
+  Buffers buf[3];
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::string err;
+  int64_t launches = 0;
+  int last_set = -1;
+  int last_mode = 0;
+  int sm_count = 0, smem_optin = 0, cc_major = 0, cc_minor = 0;
+};
+
+namespace {
+
+int fail(hs_t* h, int code, const char* fmt, ...) {
+  char b[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(b, sizeof b, fmt, ap);
+  va_end(ap);
+  if (h) h->err = b;
+  return code;
+}
+
+#define CUDA_TRY(h, expr)                                                                     \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess) return fail((h), HS_E_CUDA, "%s: %s (%s:%d)", #expr,               \
+                                       cudaGetErrorString(_e), __FILE__, __LINE__);           \
+  } while (0)
+
+bool valid_set(int set) { return set >= 0 && set <= 2; }
+
+std::string cfg_fingerprint(const hs_set_config& c) {
+  char b[160];
+  snprintf(b, sizeof b, "%d/%d/%d/%d%d%d%d", c.fors_trees_per_set, c.fors_sets_fused, c.fors_relax, c.variant[0],
+           c.variant[1], c.variant[2], c.variant[3]);
+  return b;
+}
+
+void drop_graphs(hs_t* h) {
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+  h->graphs.clear();
+}
+
+int check_layout(hs_t* h, int set, const hs_set_config& c) {
+  const SetInfo& I = kInfo[set];
+  if (c.fors_trees_per_set < 1 || c.fors_sets_fused < 1)
+    return fail(h, HS_E_CONFIG, "fusion counts must be positive");
+  const int lanes = c.fors_trees_per_set * (c.fors_relax ? I.t / 2 : I.t);
+  if (lanes > 1024) return fail(h, HS_E_CONFIG, "layout needs %d lanes; blocks hold at most 1024", lanes);
+  if (c.fors_trees_per_set * c.fors_sets_fused > I.k)
+    return fail(h, HS_E_CONFIG, "layout holds more than k=%d trees per CTA", I.k);
+  size_t smem = fors_smem(set, c.fors_trees_per_set, c.fors_sets_fused, c.fors_relax);
+  if (h && smem > (size_t)h->smem_optin)
+    return fail(h, HS_E_CONFIG, "layout needs %zu shared bytes; device opt-in limit is %d", smem, h->smem_optin);
+  for (int i = 0; i < 4; i++)
+    if (c.variant[i] != 0 && c.variant[i] != 1) return fail(h, HS_E_CONFIG, "variant must be 0 or 1");
+  if (c.chunk < 1) return fail(h, HS_E_CONFIG, "chunk must be >= 1");
+  return HS_OK;
+}
+
+int ensure_capacity(hs_t* h, int set, uint32_t count, size_t msg_bytes) {
+  const SetInfo& I = kInfo[set];
+  Buffers& B = h->buf[set];
+  void* before[9] = {B.msgs, B.offs, B.keyidx, B.optrand, B.sigs, B.plans, B.idx, B.roots, B.froots};
+  CUDA_TRY(h, grow(B.msgs, B.msgs_cap, std::max(msg_bytes, (size_t)1)));
+  CUDA_TRY(h, grow(B.offs, B.offs_cap, (size_t)count + 1));
+  CUDA_TRY(h, grow(B.keyidx, B.keyidx_cap, (size_t)count));
+  CUDA_TRY(h, grow(B.optrand, B.optrand_cap, (size_t)count * I.n));
+  CUDA_TRY(h, grow(B.sigs, B.sigs_cap, (size_t)count * I.sig_bytes));
+  CUDA_TRY(h, grow(B.plans, B.plans_cap, (size_t)count));
+  CUDA_TRY(h, grow(B.idx, B.idx_cap, (size_t)count * I.k));
+  CUDA_TRY(h, grow(B.roots, B.roots_cap, (size_t)count * (I.d + 1) * 8));
+  CUDA_TRY(h, grow(B.froots, B.froots_cap, (size_t)count * I.k * 8));
+  void* after[9] = {B.msgs, B.offs, B.keyidx, B.optrand, B.sigs, B.plans, B.idx, B.roots, B.froots};
+  if (std::memcmp(before, after, sizeof before) != 0) {
+    B.gen++;
+    drop_graphs(h);
+  }
+  return HS_OK;
+}
+
+LaunchArgs make_args(hs_t* h, int set, uint32_t count) {
+  SetState& St = h->sets[set];
+  Buffers& B = h->buf[set];
+  LaunchArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.keys = St.keys;
+  a.nkeys = St.nkeys;
+  a.msgs = B.msgs;
+  a.offs = B.offs;
+  a.key_idx = St.has_keyidx ? B.keyidx : nullptr;
+  a.opt_rand = St.has_optrand ? B.optrand : nullptr;
+  a.count = count;
+  a.sigs = B.sigs;
+  a.plans = B.plans;
+  a.indices = B.idx;
+  a.roots = B.roots;
+  a.fors_roots = B.froots;
+  a.fors_trees_per_set = St.cfg.fors_trees_per_set;
+  a.fors_sets_fused = St.cfg.fors_sets_fused;
+  a.fors_relax = St.cfg.fors_relax;
+  return a;
+}
+
+// Issue the signing DAG.  `capture` selects external (graph-visible) timing
+// events; `serial` puts every kernel on s0 back to back.
+cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool serial) {
+  const hs_set_config& c = h->sets[set].cfg;
+  auto rec = [&](int i, cudaStream_t s) {
+    return capture ? cudaEventRecordWithFlags(h->ev[i], s, cudaEventRecordExternal) : cudaEventRecord(h->ev[i], s);
+  };
+  cudaError_t e;
+#define TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
+  TRY(rec(0, h->s0));
+  TRY(launch(set, K_PREP, c.variant[3], a, h->s0));
+  TRY(rec(1, h->s0));
+  if (serial) {
+    TRY(launch(set, K_FORS, c.variant[0], a, h->s0));
+    TRY(launch(set, K_FORSPK, c.variant[0], a, h->s0));
+    TRY(rec(2, h->s0));
+    TRY(launch(set, K_TREE, c.variant[1], a, h->s0));
+    TRY(rec(3, h->s0));
+    TRY(rec(5, h->s0));
+    TRY(launch(set, K_WOTS, c.variant[2], a, h->s0));
+    TRY(rec(4, h->s0));
+  } else {
+    TRY(cudaEventRecord(h->fork, h->s0));
+    TRY(cudaStreamWaitEvent(h->s1, h->fork, 0));
+    TRY(launch(set, K_FORS, c.variant[0], a, h->s1));
+    TRY(launch(set, K_FORSPK, c.variant[0], a, h->s1));
+    TRY(rec(2, h->s1));
+    TRY(cudaEventRecord(h->join, h->s1));
+    TRY(launch(set, K_TREE, c.variant[1], a, h->s0));
+    TRY(rec(3, h->s0));
+    TRY(cudaStreamWaitEvent(h->s0, h->join, 0));
+    TRY(rec(5, h->s0));
+    TRY(launch(set, K_WOTS, c.variant[2], a, h->s0));
+    TRY(rec(4, h->s0));
+  }
+#undef TRY
+  h->launches += 5;
+  return cudaSuccess;
+}
+
+int run_batch(hs_t* h, int set, uint32_t count, int mode) {
+  SetState& St = h->sets[set];
+  if (count == 0) return HS_OK;
+  const LaunchArgs a = make_args(h, set, count);
+  const bool serial = mode == 1;
+  h->last_set = set;
+  h->last_mode = mode;
+  if (!serial && St.cfg.use_graph) {
+    GraphKey key{set, count, St.has_keyidx ? 1 : 0, St.has_optrand ? 1 : 0, h->buf[set].gen,
+                 cfg_fingerprint(St.cfg) + "/" + std::to_string((uintptr_t)St.keys)};
+    auto it = h->graphs.find(key);
+    if (it == h->graphs.end()) {
+      cudaGraph_t g;
+      CUDA_TRY(h, cudaStreamBeginCapture(h->s0, cudaStreamCaptureModeThreadLocal));
+      cudaError_t e = enqueue(h, set, a, true, false);
+      cudaError_t e2 = cudaStreamEndCapture(h->s0, &g);
+      if (e != cudaSuccess) return fail(h, HS_E_CUDA, "capture: %s", cudaGetErrorString(e));
+      if (e2 != cudaSuccess) return fail(h, HS_E_CUDA, "end capture: %s", cudaGetErrorString(e2));
+      cudaGraphExec_t ex;
+      CUDA_TRY(h, cudaGraphInstantiate(&ex, g, 0));
+      cudaGraphDestroy(g);
+      h->launches -= 5;  // capture does not launch
+      it = h->graphs.emplace(key, ex).first;
+    }
+    CUDA_TRY(h, cudaGraphLaunch(it->second, h->s0));
+    h->launches += 5;
+  } else {
+    CUDA_TRY(h, enqueue(h, set, a, false, serial));
+  }
+  return HS_OK;
+}
+
+int stage_inputs(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, const uint32_t* key_idx,
+                 const uint8_t* opt_rand, uint32_t first, uint32_t count) {
+  const SetInfo& I = kInfo[set];
+  SetState& St = h->sets[set];
+  Buffers& B = h->buf[set];
+  const uint64_t base = offs[first];
+  const uint64_t bytes = offs[first + count] - base;
+  int rc = ensure_capacity(h, set, count, (size_t)bytes);
+  if (rc) return rc;
+  CUDA_TRY(h, grow_host(B.h_offs, B.h_offs_cap, (size_t)count + 1));
+  CUDA_TRY(h, grow_host(B.h_msgs, B.h_msgs_cap, std::max((size_t)bytes, (size_t)1)));
+  for (uint32_t i = 0; i <= count; i++) B.h_offs[i] = offs[first + i] - base;
+  if (bytes) std::memcpy(B.h_msgs, msgs + base, (size_t)bytes);
+  CUDA_TRY(h, cudaMemcpyAsync(B.offs, B.h_offs, ((size_t)count + 1) * 8, cudaMemcpyHostToDevice, h->s0));
+  if (bytes) CUDA_TRY(h, cudaMemcpyAsync(B.msgs, B.h_msgs, (size_t)bytes, cudaMemcpyHostToDevice, h->s0));
+  St.has_keyidx = key_idx != nullptr;
+  St.has_optrand = opt_rand != nullptr;
+  if (key_idx) {
+    for (uint32_t i = 0; i < count; i++)
+      if (key_idx[first + i] >= St.nkeys)
+        return fail(h, HS_E_USAGE, "key_idx[%u]=%u outside the uploaded key table (%u keys)", first + i,
+                    key_idx[first + i], St.nkeys);
+    CUDA_TRY(h, cudaMemcpyAsync(B.keyidx, key_idx + first, (size_t)count * 4, cudaMemcpyHostToDevice, h->s0));
+  }
+  if (opt_rand)
+    CUDA_TRY(h, cudaMemcpyAsync(B.optrand, opt_rand + (size_t)first * I.n, (size_t)count * I.n,
+                                cudaMemcpyHostToDevice, h->s0));
+  St.staged = count;
+  return HS_OK;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+int hs_open(int device, hs_t** out) {
+  if (!out) return HS_E_USAGE;
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) return HS_E_CUDA;
+  if (device < 0 || device >= ndev) return HS_E_USAGE;
+  hs_t* h = new hs_ctx();
+  h->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) { delete h; return HS_E_CUDA; }
+  cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  cudaDeviceGetAttribute(&h->cc_major, cudaDevAttrComputeCapabilityMajor, device);
+  cudaDeviceGetAttribute(&h->cc_minor, cudaDevAttrComputeCapabilityMinor, device);
+  if (cudaStreamCreateWithFlags(&h->s0, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->s1, cudaStreamNonBlocking) != cudaSuccess) {
+    delete h;
+    return HS_E_CUDA;
+  }
+  for (auto& ev : h->ev) cudaEventCreate(&ev);
+  cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&h->join, cudaEventDisableTiming);
+  for (int s = 0; s < 3; s++) h->sets[s].cfg = default_config(s);
+  *out = h;
+  return HS_OK;
+}
+
+void hs_close(hs_t* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  drop_graphs(h);
+  for (int s = 0; s < 3; s++) {
+    Buffers& B = h->buf[s];
+    cudaFree(B.msgs); cudaFree(B.offs); cudaFree(B.keyidx); cudaFree(B.optrand); cudaFree(B.sigs);
+    cudaFree(B.plans); cudaFree(B.idx); cudaFree(B.roots); cudaFree(B.froots);
+    cudaFreeHost(B.h_msgs); cudaFreeHost(B.h_offs); cudaFreeHost(B.h_sigs);
+    cudaFree(h->sets[s].keys);
+    cudaFree(h->sets[s].sk_raw);
+  }
+  for (auto& ev : h->ev) cudaEventDestroy(ev);
+  cudaEventDestroy(h->fork);
+  cudaEventDestroy(h->join);
+  cudaStreamDestroy(h->s0);
+  cudaStreamDestroy(h->s1);
+  delete h;
+}
+
+const char* hs_last_error(const hs_t* h) { return h ? h->err.c_str() : "null handle"; }
+
+int hs_device_info(hs_t* h, int32_t* sm, int32_t* smem, int32_t* ma, int32_t* mi) {
+  if (!h) return HS_E_USAGE;
+  if (sm) *sm = h->sm_count;
+  if (smem) *smem = h->smem_optin;
+  if (ma) *ma = h->cc_major;
+  if (mi) *mi = h->cc_minor;
+  return HS_OK;
+}
+
+int hs_params(int set, int32_t* fields, int cap) {
+  if (!valid_set(set) || !fields) return HS_E_USAGE;
+  const int nf = (int)(sizeof(SetInfo) / sizeof(int));
+  const int* src = reinterpret_cast<const int*>(&kInfo[set]);
+  int m = std::min(cap, nf);
+  for (int i = 0; i < m; i++) fields[i] = src[i];
+  return m;
+}
+
+int hs_config_get(hs_t* h, int set, hs_set_config* cfg) {
+  if (!h || !valid_set(set) || !cfg) return fail(h, HS_E_USAGE, "bad arguments");
+  *cfg = h->sets[set].cfg;
+  return HS_OK;
+}
+
+int hs_config_set(hs_t* h, int set, const hs_set_config* cfg) {
+  if (!h || !valid_set(set) || !cfg) return fail(h, HS_E_USAGE, "bad arguments");
+  int rc = check_layout(h, set, *cfg);
+  if (rc) return rc;
+  h->sets[set].cfg = *cfg;
+  return HS_OK;
+}
+
+int64_t hs_fors_smem_bytes(int set, int32_t nt, int32_t f, int32_t relax) {
+  if (!valid_set(set) || nt < 1 || f < 1) return -1;
+  return (int64_t)fors_smem(set, nt, f, relax);
+}
+
+int hs_keys_upload(hs_t* h, int set, const uint8_t* sks, uint32_t nkeys) {
+  if (!h || !valid_set(set) || (!sks && nkeys)) return fail(h, HS_E_USAGE, "bad arguments");
+  if (nkeys == 0) return fail(h, HS_E_USAGE, "at least one key is required");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  const SetInfo& I = kInfo[set];
+  SetState& St = h->sets[set];
+  KeyDev* old = St.keys;
+  CUDA_TRY(h, grow(St.keys, St.keys_cap, nkeys));
+  if (old != St.keys) drop_graphs(h);
+  CUDA_TRY(h, grow(St.sk_raw, St.sk_raw_cap, (size_t)nkeys * 4 * I.n));
+  CUDA_TRY(h, cudaMemcpyAsync(St.sk_raw, sks, (size_t)nkeys * 4 * I.n, cudaMemcpyHostToDevice, h->s0));
+  LaunchArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.sk_bytes = St.sk_raw;
+  a.nkeys = nkeys;
+  a.keys_out = St.keys;
+  CUDA_TRY(h, launch(set, K_KEYSETUP, St.cfg.variant[3], a, h->s0));
+  h->launches++;
+  CUDA_TRY(h, cudaStreamSynchronize(h->s0));
+  St.nkeys = nkeys;
+  return HS_OK;
+}
+
+int hs_keygen_batch(hs_t* h, int set, const uint8_t* seeds, uint32_t nkeys, uint8_t* sks_out) {
+  if (!h || !valid_set(set) || !seeds || !sks_out) return fail(h, HS_E_USAGE, "bad arguments");
+  if (nkeys == 0) return HS_OK;
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  const SetInfo& I = kInfo[set];
+  std::vector<uint8_t> padded((size_t)nkeys * 4 * I.n, 0);
+  for (uint32_t i = 0; i < nkeys; i++) std::memcpy(&padded[(size_t)i * 4 * I.n], seeds + (size_t)i * 3 * I.n, 3 * I.n);
+  uint8_t *d_in = nullptr, *d_out = nullptr;
+  KeyDev* d_keys = nullptr;
+  int rc = HS_OK;
+  cudaError_t e = cudaMalloc(&d_in, padded.size());
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, padded.size());
+  if (e == cudaSuccess) e = cudaMalloc(&d_keys, (size_t)nkeys * sizeof(KeyDev));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_in, padded.data(), padded.size(), cudaMemcpyHostToDevice, h->s0);
+  LaunchArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.sk_bytes = d_in;
+  a.nkeys = nkeys;
+  a.keys_out = d_keys;
+  a.keys = d_keys;
+  a.sk_out = d_out;
+  const hs_set_config& c = h->sets[set].cfg;
+  if (e == cudaSuccess) e = launch(set, K_KEYSETUP, c.variant[3], a, h->s0);
+  if (e == cudaSuccess) e = launch(set, K_KEYGEN, c.variant[1], a, h->s0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(sks_out, d_out, padded.size(), cudaMemcpyDeviceToHost, h->s0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->s0);
+  h->launches += 2;
+  if (e != cudaSuccess) rc = fail(h, HS_E_CUDA, "keygen: %s", cudaGetErrorString(e));
+  cudaFree(d_in);
+  cudaFree(d_out);
+  cudaFree(d_keys);
+  return rc;
+}
+
+int hs_stage(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, const uint32_t* key_idx,
+             const uint8_t* opt_rand, uint32_t count) {
+  if (!h || !valid_set(set) || !offs || (!msgs && count && offs[count] != offs[0]))
+    return fail(h, HS_E_USAGE, "bad arguments");
+  if (h->sets[set].nkeys == 0) return fail(h, HS_E_NOKEYS, "no keys uploaded for this parameter set");
+  if (offs[count] < offs[0]) return fail(h, HS_E_USAGE, "offsets must be non-decreasing");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  return stage_inputs(h, set, msgs, offs, key_idx, opt_rand, 0, count);
+}
+
+int hs_run(hs_t* h, int set, uint32_t count, int mode) {
+  if (!h || !valid_set(set)) return fail(h, HS_E_USAGE, "bad arguments");
+  if (count > h->sets[set].staged) return fail(h, HS_E_USAGE, "count exceeds the staged batch");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  return run_batch(h, set, count, mode);
+}
+
+int hs_sync(hs_t* h) {
+  if (!h) return HS_E_USAGE;
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  CUDA_TRY(h, cudaStreamSynchronize(h->s0));
+  CUDA_TRY(h, cudaStreamSynchronize(h->s1));
+  return HS_OK;
+}
+
+int hs_fetch(hs_t* h, int set, uint32_t first, uint32_t count, uint8_t* sigs) {
+  if (!h || !valid_set(set) || !sigs) return fail(h, HS_E_USAGE, "bad arguments");
+  if ((uint64_t)first + count > h->sets[set].staged) return fail(h, HS_E_USAGE, "range exceeds the staged batch");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  const size_t sb = (size_t)kInfo[set].sig_bytes;
+  CUDA_TRY(h, cudaMemcpyAsync(sigs, h->buf[set].sigs + first * sb, count * sb, cudaMemcpyDeviceToHost, h->s0));
+  CUDA_TRY(h, cudaStreamSynchronize(h->s0));
+  return HS_OK;
+}
+
+int hs_sign_batch(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, const uint32_t* key_idx,
+                  const uint8_t* opt_rand, uint32_t count, uint8_t* sigs) {
+  if (!h || !valid_set(set) || !offs || (count && !sigs)) return fail(h, HS_E_USAGE, "bad arguments");
+  if (count == 0) return HS_OK;
+  if (!msgs && offs[count] != offs[0]) return fail(h, HS_E_USAGE, "null message buffer");
+  for (uint32_t i = 0; i < count; i++)
+    if (offs[i + 1] < offs[i]) return fail(h, HS_E_USAGE, "offsets must be non-decreasing");
+  if (h->sets[set].nkeys == 0) return fail(h, HS_E_NOKEYS, "no keys uploaded for this parameter set");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  const size_t sb = (size_t)kInfo[set].sig_bytes;
+  const uint32_t chunk = (uint32_t)std::max(1, h->sets[set].cfg.chunk);
+  const bool direct = is_pinned(sigs);
+  Buffers& B = h->buf[set];
+  float total_ms = 0.f, part[4] = {0, 0, 0, 0};
+  for (uint32_t first = 0; first < count; first += chunk) {
+    const uint32_t cn = std::min(chunk, count - first);
+    int rc = stage_inputs(h, set, msgs, offs, key_idx, opt_rand, first, cn);
+    if (rc) return rc;
+    rc = run_batch(h, set, cn, 0);
+    if (rc) return rc;
+    if (direct) {
+      CUDA_TRY(h, cudaMemcpyAsync(sigs + first * sb, B.sigs, cn * sb, cudaMemcpyDeviceToHost, h->s0));
+      CUDA_TRY(h, cudaStreamSynchronize(h->s0));
+    } else {
+      CUDA_TRY(h, grow_host(B.h_sigs, B.h_sigs_cap, (size_t)cn * sb));
+      CUDA_TRY(h, cudaMemcpyAsync(B.h_sigs, B.sigs, cn * sb, cudaMemcpyDeviceToHost, h->s0));
+      CUDA_TRY(h, cudaStreamSynchronize(h->s0));
+      std::memcpy(sigs + first * sb, B.h_sigs, cn * sb);
+    }
+    float ms[5];
+    if (hs_timings(h, ms, 5) == 5) {
+      total_ms += ms[0];
+      for (int i = 0; i < 4; i++) part[i] += ms[1 + i];
+    }
+  }
+  return HS_OK;
+}
+
+int hs_verify_batch(hs_t* h, int set, const uint8_t* pks, uint32_t nkeys, const uint8_t* msgs, const uint64_t* offs,
+                    const uint32_t* key_idx, const uint8_t* sigs, uint32_t count, uint8_t* ok) {
+  if (!h || !valid_set(set) || !pks || !offs || (count && (!sigs || !ok)) || nkeys == 0)
+    return fail(h, HS_E_USAGE, "bad arguments");
+  if (count == 0) return HS_OK;
+  for (uint32_t i = 0; i < count; i++) {
+    if (offs[i + 1] < offs[i]) return fail(h, HS_E_USAGE, "offsets must be non-decreasing");
+    if (key_idx && key_idx[i] >= nkeys) return fail(h, HS_E_USAGE, "key_idx[%u] out of range", i);
+  }
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  const SetInfo& I = kInfo[set];
+  const uint64_t base = offs[0], mbytes = offs[count] - offs[0];
+  std::vector<uint64_t> ro(count + 1);
+  for (uint32_t i = 0; i <= count; i++) ro[i] = offs[i] - base;
+  uint8_t *d_pks = nullptr, *d_msgs = nullptr, *d_sigs = nullptr, *d_ok = nullptr;
+  uint64_t* d_offs = nullptr;
+  uint32_t* d_kidx = nullptr;
+  cudaError_t e = cudaMalloc(&d_pks, (size_t)nkeys * 2 * I.n);
+  if (e == cudaSuccess) e = cudaMalloc(&d_msgs, std::max<size_t>(mbytes, 1));
+  if (e == cudaSuccess) e = cudaMalloc(&d_sigs, (size_t)count * I.sig_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&d_ok, count);
+  if (e == cudaSuccess) e = cudaMalloc(&d_offs, ((size_t)count + 1) * 8);
+  if (e == cudaSuccess && key_idx) e = cudaMalloc(&d_kidx, (size_t)count * 4);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_pks, pks, (size_t)nkeys * 2 * I.n, cudaMemcpyHostToDevice, h->s0);
+  if (e == cudaSuccess && mbytes) e = cudaMemcpyAsync(d_msgs, msgs + base, mbytes, cudaMemcpyHostToDevice, h->s0);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_sigs, sigs, (size_t)count * I.sig_bytes, cudaMemcpyHostToDevice, h->s0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_offs, ro.data(), ro.size() * 8, cudaMemcpyHostToDevice, h->s0);
+  if (e == cudaSuccess && key_idx)
+    e = cudaMemcpyAsync(d_kidx, key_idx, (size_t)count * 4, cudaMemcpyHostToDevice, h->s0);
+  LaunchArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.pks = d_pks;
+  a.nkeys = nkeys;
+  a.msgs = d_msgs;
+  a.offs = d_offs;
+  a.key_idx = d_kidx;
+  a.vsigs = d_sigs;
+  a.ok = d_ok;
+  a.count = count;
+  if (e == cudaSuccess) e = launch(set, K_VERIFY, h->sets[set].cfg.variant[2], a, h->s0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(ok, d_ok, count, cudaMemcpyDeviceToHost, h->s0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->s0);
+  h->launches++;
+  cudaFree(d_pks); cudaFree(d_msgs); cudaFree(d_sigs); cudaFree(d_ok); cudaFree(d_offs); cudaFree(d_kidx);
+  if (e != cudaSuccess) return fail(h, HS_E_CUDA, "verify: %s", cudaGetErrorString(e));
+  return HS_OK;
+}
+
+int hs_timings(hs_t* h, float* ms, int cap) {
+  if (!h || !ms || cap < 1) return HS_E_USAGE;
+  if (h->last_set < 0) return 0;
+  cudaSetDevice(h->device);
+  if (cudaEventSynchronize(h->ev[4]) != cudaSuccess) return fail(h, HS_E_CUDA, "timing events not complete");
+  float v[5] = {0, 0, 0, 0, 0};
+  cudaEventElapsedTime(&v[0], h->ev[0], h->ev[4]);
+  cudaEventElapsedTime(&v[1], h->ev[0], h->ev[1]);
+  cudaEventElapsedTime(&v[2], h->ev[1], h->ev[2]);
+  if (h->last_mode == 1) cudaEventElapsedTime(&v[3], h->ev[2], h->ev[3]);
+  else cudaEventElapsedTime(&v[3], h->ev[1], h->ev[3]);
+  cudaEventElapsedTime(&v[4], h->ev[5], h->ev[4]);
+  int m = std::min(cap, 5);
+  for (int i = 0; i < m; i++) ms[i] = v[i];
+  return m;
+}
+
+int64_t hs_launch_count(hs_t* h) { return h ? h->launches : -1; }
+
+void* hs_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, std::max<size_t>(bytes, 1)) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void hs_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

@@ -1,0 +1,30 @@
+// hs_internal.h -- glue between the host runtime (hs_api.cu) and the
+// per-set kernel objects (hs_set.cu compiled with -DHS_SET=0/1/2).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+namespace hs {
+
+struct LaunchArgs;
+
+enum KernelId : int {
+  K_KEYSETUP = 0,
+  K_PREP = 1,
+  K_FORS = 2,
+  K_FORSPK = 3,
+  K_TREE = 4,
+  K_WOTS = 5,
+  K_KEYGEN = 6,
+  K_VERIFY = 7,
+};
+
+// variant: 0 = Native, 1 = Imad (sha256.cuh)
+template <int S>
+cudaError_t launch_kernel(int which, int variant, const LaunchArgs& a, cudaStream_t s);
+
+template <int S>
+size_t fors_smem_bytes(int trees_per_set, int sets_fused, int relax);
+
+}  // namespace hs

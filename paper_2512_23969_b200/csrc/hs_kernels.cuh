@@ -1,0 +1,728 @@
+// hs_kernels.cuh -- the B200 signing kernels (templated on parameter set S
+// and SHA-256 arithmetic path V).
+//
+//   key_setup   per key: PK.seed midstate, HMAC ipad/opad midstates
+//               (hashes.py:79-88 precomputation, done once per key on device)
+//   msg_prep    per message: R = PRF_msg, H_msg, MGF1, tree/leaf/FORS indices
+//               (hashes.py:152-191, sigcore.py:75-121)
+//   fors_sign   FORS_Sign with the paper's Tree Fusion: a CTA owns F fused
+//               sets of N_tree trees (vexec.py:319-473, FusedSetLayout
+//               vexec.py:130-181, Relax vexec.py:115-127)
+//   fors_pk     T_k over the k FORS roots (vexec.py:476-481)
+//   tree_sign   TREE_Sign: one thread per hypertree leaf runs the full WOTS
+//               leaf (wots.py:119-143); the subtree is reduced with warp
+//               shuffles (vexec.py:492-551 / oracle.py:27-63)
+//   wots_sign   WOTS+_Sign: one thread per (layer, chain) (parallel.py:31-59)
+//   keygen_root root of layer d-1, tree 0 (oracle.py:216-226)
+//   verify      one warp per message (sigcore.py:181-221)
+//
+// Every output byte equals the reference's sigcore.sign for the same inputs.
+#pragma once
+#include <cstdint>
+
+#include "hs_params.cuh"
+#include "sha256.cuh"
+
+namespace hs {
+
+// Per-key device record (built by key_setup from sk = sk_seed||sk_prf||pk_seed||pk_root).
+struct KeyDev {
+  uint32_t sk_seed[8];
+  uint32_t sk_prf[8];
+  uint32_t pk_seed[8];
+  uint32_t pk_root[8];
+  uint32_t thash_mid[8];  // compress(IV, pk_seed || 0^(64-n))
+  uint32_t hmac_i[8];     // compress(IV, (sk_prf||0) ^ 0x36..)
+  uint32_t hmac_o[8];     // compress(IV, (sk_prf||0) ^ 0x5c..)
+};
+
+struct MsgPlan {
+  uint64_t tree;   // bottom-layer tree index (masked to h - h/d bits)
+  uint32_t leaf;   // bottom-layer leaf index
+  uint32_t key;    // key table row
+};
+
+// Everything a launch needs; device pointers only.
+struct LaunchArgs {
+  const KeyDev* keys;
+  KeyDev* keys_out;          // key_setup / keygen target
+  const uint8_t* sk_bytes;   // key_setup input (nkeys * 4n) or keygen seeds (nkeys * 3n)
+  uint32_t nkeys;
+  const uint8_t* msgs;
+  const uint64_t* offs;
+  const uint32_t* key_idx;   // nullptr = key 0
+  const uint8_t* opt_rand;   // nullptr = pk_seed (sigcore.py:162-163)
+  uint32_t count;
+  uint8_t* sigs;
+  MsgPlan* plans;
+  uint16_t* indices;         // count * k
+  uint32_t* roots;           // count * (d+1) * 8 words; slot 0 = FORS pk, slot l+1 = root of layer l
+  uint32_t* fors_roots;      // count * k * 8 words
+  uint8_t* sk_out;           // keygen output (nkeys * 4n)
+  const uint8_t* pks;        // verify: nkeys * 2n (pk_seed || pk_root)
+  const uint8_t* vsigs;      // verify: count * sig_bytes
+  uint8_t* ok;               // verify: count flags
+  int fors_trees_per_set;    // N_tree
+  int fors_sets_fused;       // F
+  int fors_relax;
+};
+
+__device__ __forceinline__ uint64_t shr64(uint64_t x, int s) { return s >= 64 ? 0ull : (x >> s); }
+
+__device__ __forceinline__ void store_be(uint8_t* p, uint32_t w) { *reinterpret_cast<uint32_t*>(p) = bswap32(w); }
+
+template <int NW>
+__device__ __forceinline__ void store_node(uint8_t* p, const uint32_t* x) {
+#pragma unroll
+  for (int j = 0; j < NW; j++) store_be(p + 4 * j, x[j]);
+}
+
+__device__ __forceinline__ uint32_t load_be(const uint8_t* p) {
+  return ((uint32_t)p[0] << 24) | ((uint32_t)p[1] << 16) | ((uint32_t)p[2] << 8) | p[3];
+}
+
+// ---------------------------------------------------------------------------
+// key_setup: one thread per key
+// ---------------------------------------------------------------------------
+template <int S, class V>
+__global__ void key_setup_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.nkeys) return;
+  const uint8_t* sk = a.sk_bytes + (size_t)i * Pr::sk_bytes;
+  KeyDev kd;
+  for (int j = 0; j < 8; j++) {
+    kd.sk_seed[j] = j < Pr::NW ? load_be(sk + 4 * j) : 0u;
+    kd.sk_prf[j] = j < Pr::NW ? load_be(sk + Pr::n + 4 * j) : 0u;
+    kd.pk_seed[j] = j < Pr::NW ? load_be(sk + 2 * Pr::n + 4 * j) : 0u;
+    kd.pk_root[j] = j < Pr::NW ? load_be(sk + 3 * Pr::n + 4 * j) : 0u;
+  }
+  uint32_t W[16];
+  for (int j = 0; j < 8; j++) kd.thash_mid[j] = IVc(j);
+  for (int j = 0; j < 16; j++) W[j] = j < Pr::NW ? kd.pk_seed[j] : 0u;
+  compress<V>(kd.thash_mid, W);
+  for (int j = 0; j < 8; j++) kd.hmac_i[j] = IVc(j);
+  for (int j = 0; j < 16; j++) W[j] = (j < Pr::NW ? kd.sk_prf[j] : 0u) ^ 0x36363636u;
+  compress<V>(kd.hmac_i, W);
+  for (int j = 0; j < 8; j++) kd.hmac_o[j] = IVc(j);
+  for (int j = 0; j < 16; j++) W[j] = (j < Pr::NW ? kd.sk_prf[j] : 0u) ^ 0x5c5c5c5cu;
+  compress<V>(kd.hmac_o, W);
+  a.keys_out[i] = kd;
+}
+
+// ---------------------------------------------------------------------------
+// msg_prep: one thread per message (hashes.py:152-191, sigcore.py:75-90)
+// ---------------------------------------------------------------------------
+template <int S, class V>
+__global__ void msg_prep_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  constexpr int n = Pr::n;
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.count) return;
+  const uint32_t key = a.key_idx ? a.key_idx[i] : 0u;
+  const KeyDev& K = a.keys[key];
+  const uint8_t* msg = a.msgs + a.offs[i];
+  const uint64_t mlen = a.offs[i + 1] - a.offs[i];
+
+  // R = HMAC-SHA-256(sk_prf, opt_rand || msg)[:n]
+  ByteSha<V> hs;
+  uint32_t inner[8], R[8];
+  hs.init_mid(K.hmac_i, 64);
+  if (a.opt_rand) hs.bytes(a.opt_rand + (size_t)i * n, n);
+  else hs.words(K.pk_seed, n);
+  hs.bytes(msg, mlen);
+  hs.final(inner);
+  hs.init_mid(K.hmac_o, 64);
+  hs.words(inner, 32);
+  hs.final(R);
+  uint8_t* sig = a.sigs + (size_t)i * Pr::sig_bytes;
+  store_node<Pr::NW>(sig, R);
+
+  // H_msg: MGF1(R || PK.seed || SHA-256(R || PK.seed || PK.root || M), digest_bytes)
+  uint32_t dig0[8];
+  hs.init_iv();
+  hs.words(R, n);
+  hs.words(K.pk_seed, n);
+  hs.words(K.pk_root, n);
+  hs.bytes(msg, mlen);
+  hs.final(dig0);
+  uint8_t dg[64];
+  constexpr int nctr = (Pr::digest_bytes + 31) / 32;
+  for (int c = 0; c < nctr; c++) {
+    uint32_t o[8];
+    hs.init_iv();
+    hs.words(R, n);
+    hs.words(K.pk_seed, n);
+    hs.words(dig0, 32);
+    hs.word((uint32_t)c);
+    hs.final(o);
+    for (int j = 0; j < 32; j++) dg[32 * c + j] = (uint8_t)(o[j >> 2] >> (24 - 8 * (j & 3)));
+  }
+  uint64_t tree = 0;
+  for (int j = 0; j < Pr::tree_bytes; j++) tree = (tree << 8) | dg[Pr::fors_msg_bytes + j];
+  if (Pr::tree_bits < 64) tree &= (1ull << (Pr::tree_bits < 64 ? Pr::tree_bits : 63)) - 1ull;
+  uint32_t leaf = 0;
+  for (int j = 0; j < Pr::leaf_bytes; j++) leaf = (leaf << 8) | dg[Pr::fors_msg_bytes + Pr::tree_bytes + j];
+  leaf &= (1u << Pr::leaf_bits) - 1u;
+  MsgPlan pl;
+  pl.tree = tree;
+  pl.leaf = leaf;
+  pl.key = key;
+  a.plans[i] = pl;
+  // FORS indices, LSB-first bit order within each byte (sigcore.py:75-90)
+  int off = 0;
+  for (int g = 0; g < Pr::k; g++) {
+    uint32_t v = 0;
+    for (int j = 0; j < Pr::log_t; j++, off++) v |= (uint32_t)((dg[off >> 3] >> (off & 7)) & 1) << j;
+    a.indices[(size_t)i * Pr::k + g] = (uint16_t)v;
+  }
+}
+
+// layer schedule (sigcore.py:107-121)
+template <int S>
+__device__ __forceinline__ void layer_coords(const MsgPlan& pl, int layer, uint64_t& tree, uint32_t& leaf) {
+  using Pr = P<S>;
+  if (layer == 0) {
+    tree = pl.tree;
+    leaf = pl.leaf;
+  } else {
+    leaf = (uint32_t)(shr64(pl.tree, Pr::hp * (layer - 1)) & (uint64_t)(Pr::leaves - 1));
+    tree = shr64(pl.tree, Pr::hp * layer);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// One WOTS+ leaf (wots.py:119-143): wots_len chains of PRF + (w-1) F, then
+// T_len over the chain ends streamed through this thread's smem column.
+// ---------------------------------------------------------------------------
+template <int S, class V>
+__device__ __forceinline__ void wots_leaf(const KeyDev& K, uint32_t layer, uint64_t tree, uint32_t leaf,
+                                          uint32_t* column, int stride, uint32_t out[8]) {
+  using Pr = P<S>;
+  constexpr int NW = Pr::NW;
+  uint32_t mid[8], sks[NW];
+#pragma unroll
+  for (int j = 0; j < 8; j++) mid[j] = K.thash_mid[j];
+#pragma unroll
+  for (int j = 0; j < NW; j++) sks[j] = K.sk_seed[j];
+  TStream<V> ts;
+  ts.begin(mid, make_adrs(layer, tree, ADDR_WOTS_PK, leaf, 0, 0), column, stride);
+  Adrs wa = make_adrs(layer, tree, ADDR_WOTS, leaf, 0, 0);
+#pragma unroll 1
+  for (int i = 0; i < Pr::wots_len; i++) {
+    uint32_t st[8];
+    adrs_set_chain_hash(wa, (uint32_t)i, 0);
+    prf_reg<V, NW>(st, sks, wa);
+    uint32_t x[NW];
+#pragma unroll
+    for (int j = 0; j < NW; j++) x[j] = st[j];
+#pragma unroll 1
+    for (int s = 0; s < Pr::w - 1; s++) {
+      adrs_set_chain_hash(wa, (uint32_t)i, (uint32_t)s);
+      thash_reg<V, NW>(st, mid, wa, x);
+#pragma unroll
+      for (int j = 0; j < NW; j++) x[j] = st[j];
+    }
+    ts.template push_node<NW>(x);
+  }
+  ts.finish(22u + (uint32_t)(Pr::wots_len * Pr::n));
+#pragma unroll
+  for (int j = 0; j < 8; j++) out[j] = ts.st[j];
+}
+
+// ---------------------------------------------------------------------------
+// TREE_Sign: thread = (message, layer, leaf); leaves of a subtree sit in
+// consecutive lanes of one warp and are reduced with shuffles.
+// ---------------------------------------------------------------------------
+constexpr int kTreeBlock = 128;
+
+template <int S, class V>
+__global__ void __launch_bounds__(kTreeBlock) tree_sign_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  constexpr int NW = Pr::NW;
+  __shared__ uint32_t tbuf[16 * kTreeBlock];
+  const uint64_t per_msg = (uint64_t)Pr::d * Pr::leaves;
+  const uint64_t gid = (uint64_t)blockIdx.x * kTreeBlock + threadIdx.x;
+  const bool valid = gid < (uint64_t)a.count * per_msg;
+  const uint32_t msg = valid ? (uint32_t)(gid / per_msg) : 0u;
+  const uint32_t rem = (uint32_t)(gid % per_msg);
+  const uint32_t layer = rem / Pr::leaves;
+  const uint32_t leaf = rem % Pr::leaves;
+
+  uint32_t node[8];
+  uint64_t tree = 0;
+  uint32_t leaf_idx = 0;
+  const KeyDev* K = nullptr;
+  if (valid) {
+    const MsgPlan pl = a.plans[msg];
+    K = &a.keys[pl.key];
+    layer_coords<S>(pl, (int)layer, tree, leaf_idx);
+    wots_leaf<S, V>(*K, layer, tree, leaf, &tbuf[threadIdx.x], kTreeBlock, node);
+  }
+  uint8_t* auth = a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_ht + (size_t)layer * Pr::layer_bytes +
+                  Pr::wots_sig_bytes;
+#pragma unroll 1
+  for (int lvl = 1; lvl <= Pr::hp; lvl++) {
+    const uint32_t below = leaf >> (lvl - 1);
+    const bool holder_below = (leaf & ((1u << (lvl - 1)) - 1u)) == 0u;
+    if (valid && holder_below && below == ((leaf_idx >> (lvl - 1)) ^ 1u))
+      store_node<NW>(auth + (lvl - 1) * Pr::n, node);
+    uint32_t other[NW];
+#pragma unroll
+    for (int j = 0; j < NW; j++) other[j] = __shfl_down_sync(0xffffffffu, node[j], 1u << (lvl - 1));
+    if (valid && (leaf & ((1u << lvl) - 1u)) == 0u) {
+      uint32_t m[2 * NW];
+#pragma unroll
+      for (int j = 0; j < NW; j++) { m[j] = node[j]; m[NW + j] = other[j]; }
+      uint32_t mid[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) mid[j] = K->thash_mid[j];
+      thash_reg<V, 2 * NW>(node, mid, make_adrs(layer, tree, ADDR_HASHTREE, 0, (uint32_t)lvl, leaf >> lvl), m);
+    }
+  }
+  if (valid && leaf == 0) {
+    uint32_t* r = a.roots + ((size_t)msg * (Pr::d + 1) + layer + 1) * 8;
+#pragma unroll
+    for (int j = 0; j < NW; j++) r[j] = node[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FORS_Sign with Tree Fusion.  CTA = (message, pass); a pass owns F fused
+// sets of N_tree trees; blockDim = N_tree * t (or N_tree * t/2 with Relax,
+// where each lane builds a leaf pair in registers and stores only the
+// parent).  Levels ping-pong between two shared regions, one barrier per
+// level; each level's nodes of all fused trees are spread over every lane,
+// so one barrier covers all F sets.
+// ---------------------------------------------------------------------------
+template <int S>
+__host__ __device__ constexpr int fors_smem_words_per_tree(bool relax) {
+  // region A (t or t/4 nodes) + region B (t/2 nodes)
+  return relax ? (P<S>::t / 4 + P<S>::t / 2) * P<S>::NW : (P<S>::t + P<S>::t / 2) * P<S>::NW;
+}
+
+// FORS leaf (oracle.py:101-110): sk = PRF(adrs(height 0, index)), leaf = F(sk)
+template <int S, class V>
+__device__ __forceinline__ void fors_leaf(const uint32_t mid[8], const uint32_t* sks, Adrs& fa, uint32_t gidx,
+                                          uint32_t sk_out[8], uint32_t leaf_out[8]) {
+  constexpr int NW = P<S>::NW;
+  adrs_set_chain_hash(fa, 0, gidx);
+  prf_reg<V, NW>(sk_out, sks, fa);
+  thash_reg<V, NW>(leaf_out, mid, fa, sk_out);
+}
+
+template <int S, class V>
+__global__ void __launch_bounds__(1024) fors_sign_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  constexpr int NW = Pr::NW;
+  constexpr int t = Pr::t;
+  extern __shared__ uint32_t sm[];
+  const int ntree = a.fors_trees_per_set;
+  const int fused = a.fors_sets_fused;
+  const bool relax = a.fors_relax != 0;
+  const int tpc = ntree * fused;                       // trees per CTA
+  const int sets_total = (Pr::k + ntree - 1) / ntree;
+  const int passes = (sets_total + fused - 1) / fused;
+  const uint32_t msg = blockIdx.x / passes;
+  const int pass = blockIdx.x % passes;
+  const int g0 = pass * tpc;
+  const int ntr = min(tpc, Pr::k - g0);              // active trees in this CTA
+  if (msg >= a.count) return;
+  const int lanes_per_tree = relax ? t / 2 : t;
+  const int capA = relax ? t / 4 : t;
+  uint32_t* regA = sm;                                 // [tpc][capA][NW]
+  uint32_t* regB = sm + (size_t)tpc * capA * NW;       // [tpc][t/2][NW]
+
+  const MsgPlan pl = a.plans[msg];
+  const KeyDev& K = a.keys[pl.key];
+  uint32_t mid[8], sks[NW];
+#pragma unroll
+  for (int j = 0; j < 8; j++) mid[j] = K.thash_mid[j];
+#pragma unroll
+  for (int j = 0; j < NW; j++) sks[j] = K.sk_seed[j];
+  const uint16_t* idx = a.indices + (size_t)msg * Pr::k;
+  uint8_t* fsig = a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_fors;
+  constexpr int tree_sig = (1 + Pr::log_t) * Pr::n;    // sk || auth[log_t]
+  Adrs fa = make_adrs(0, pl.tree, ADDR_FORS_TREE, pl.leaf, 0, 0);
+
+  // ---- leaf phase (vexec.py:387-435) ----
+  const int tid = threadIdx.x;
+  const int tree_in_set = tid / lanes_per_tree;
+  const int lane_leaf = tid % lanes_per_tree;
+#pragma unroll 1
+  for (int f = 0; f < fused; f++) {
+    const int tl = f * ntree + tree_in_set;            // tree slot in this CTA
+    if (tl >= ntr) continue;
+    const int g = g0 + tl;
+    const uint32_t sel = idx[g];
+    if (!relax) {
+      uint32_t sk[8], lf[8];
+      fors_leaf<S, V>(mid, sks, fa, (uint32_t)(g * t + lane_leaf), sk, lf);
+      if ((uint32_t)lane_leaf == sel) store_node<NW>(fsig + g * tree_sig, sk);
+      uint32_t* dst = regA + ((size_t)tl * capA + lane_leaf) * NW;
+#pragma unroll
+      for (int j = 0; j < NW; j++) dst[j] = lf[j];
+    } else {
+      uint32_t sk0[8], l0[8], sk1[8], l1[8];
+      const uint32_t j2 = 2u * lane_leaf;
+      fors_leaf<S, V>(mid, sks, fa, (uint32_t)(g * t) + j2, sk0, l0);
+      fors_leaf<S, V>(mid, sks, fa, (uint32_t)(g * t) + j2 + 1u, sk1, l1);
+      if (j2 == sel) store_node<NW>(fsig + g * tree_sig, sk0);
+      if (j2 + 1u == sel) store_node<NW>(fsig + g * tree_sig, sk1);
+      if ((sel >> 1) == (uint32_t)lane_leaf) store_node<NW>(fsig + g * tree_sig + Pr::n, (sel & 1u) ? l0 : l1);
+      uint32_t m[2 * NW], par[8];
+#pragma unroll
+      for (int j = 0; j < NW; j++) { m[j] = l0[j]; m[NW + j] = l1[j]; }
+      adrs_set_chain_hash(fa, 1, (uint32_t)lane_leaf + ((uint32_t)(g * t) >> 1));
+      thash_reg<V, 2 * NW>(par, mid, fa, m);
+      uint32_t* dst = regB + ((size_t)tl * (t / 2) + lane_leaf) * NW;
+#pragma unroll
+      for (int j = 0; j < NW; j++) dst[j] = par[j];
+    }
+  }
+  __syncthreads();
+
+  // ---- reduction levels (vexec.py:437-463) ----
+  const int first = relax ? 2 : 1;
+#pragma unroll 1
+  for (int lvl = first; lvl <= Pr::log_t; lvl++) {
+    // level lvl-1 lives in A when (lvl-1) is even (no relax) ... track by parity
+    const bool src_is_A = relax ? ((lvl & 1) == 1) : ((lvl & 1) == 1);
+    const uint32_t* src = src_is_A ? regA : regB;
+    uint32_t* dst = src_is_A ? regB : regA;
+    const int src_cap = src_is_A ? capA : t / 2;
+    const int dst_cap = src_is_A ? t / 2 : capA;
+    const int per_tree = t >> lvl;
+    const int total = ntr * per_tree;
+#pragma unroll 1
+    for (int q = tid; q < total; q += blockDim.x) {
+      const int tl = q / per_tree;
+      const int j = q % per_tree;
+      const int g = g0 + tl;
+      const uint32_t* c = src + ((size_t)tl * src_cap + 2 * j) * NW;
+      uint32_t m[2 * NW];
+#pragma unroll
+      for (int w = 0; w < 2 * NW; w++) m[w] = c[w];
+      const uint32_t sel = (uint32_t)idx[g] >> (lvl - 1);
+      if ((sel >> 1) == (uint32_t)j)
+        store_node<NW>(fsig + g * tree_sig + Pr::n + (lvl - 1) * Pr::n, (sel & 1u) ? m : m + NW);
+      uint32_t par[8];
+      Adrs na = fa;
+      adrs_set_chain_hash(na, (uint32_t)lvl, (uint32_t)j + ((uint32_t)(g * t) >> lvl));
+      thash_reg<V, 2 * NW>(par, mid, na, m);
+      if (lvl == Pr::log_t) {
+        uint32_t* r = a.fors_roots + ((size_t)msg * Pr::k + g) * 8;
+#pragma unroll
+        for (int w = 0; w < NW; w++) r[w] = par[w];
+      } else {
+        uint32_t* d = dst + ((size_t)tl * dst_cap + j) * NW;
+#pragma unroll
+        for (int w = 0; w < NW; w++) d[w] = par[w];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// T_k over the k FORS roots -> roots slot 0 (vexec.py:476-481).
+constexpr int kSmallBlock = 128;
+
+template <int S, class V>
+__global__ void __launch_bounds__(kSmallBlock) fors_pk_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  constexpr int NW = Pr::NW;
+  __shared__ uint32_t tbuf[16 * kSmallBlock];
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.count) return;
+  const MsgPlan pl = a.plans[i];
+  const KeyDev& K = a.keys[pl.key];
+  uint32_t mid[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) mid[j] = K.thash_mid[j];
+  TStream<V> ts;
+  ts.begin(mid, make_adrs(0, pl.tree, ADDR_FORS_ROOTS, pl.leaf, 0, 0), &tbuf[threadIdx.x], kSmallBlock);
+  const uint32_t* fr = a.fors_roots + (size_t)i * Pr::k * 8;
+#pragma unroll 1
+  for (int g = 0; g < Pr::k; g++) {
+    uint32_t x[NW];
+#pragma unroll
+    for (int j = 0; j < NW; j++) x[j] = fr[g * 8 + j];
+    ts.template push_node<NW>(x);
+  }
+  ts.finish(22u + (uint32_t)(Pr::k * Pr::n));
+  uint32_t* r = a.roots + (size_t)i * (Pr::d + 1) * 8;
+#pragma unroll
+  for (int j = 0; j < NW; j++) r[j] = ts.st[j];
+}
+
+// ---------------------------------------------------------------------------
+// WOTS+_Sign: thread = (message, layer, chain) (parallel.py:31-59)
+// ---------------------------------------------------------------------------
+template <int S>
+__device__ __forceinline__ uint32_t wots_digit(const uint32_t* msg_w, int chain) {
+  using Pr = P<S>;
+  // base_w / checksum (wots.py:16-39); lg_w = 4, len2 = 3 for every set
+  static_assert(Pr::lg_w == 4 && Pr::len2 == 3, "digit extraction assumes w = 16");
+  if (chain < Pr::len1) return (msg_w[chain >> 3] >> (28 - 4 * (chain & 7))) & 15u;
+  uint32_t csum = 0;
+#pragma unroll
+  for (int i = 0; i < Pr::len1; i++) csum += 15u - ((msg_w[i >> 3] >> (28 - 4 * (i & 7))) & 15u);
+  csum <<= (8 - ((Pr::len2 * Pr::lg_w) % 8)) % 8;  // now a 16-bit big-endian value
+  const int c = chain - Pr::len1;                  // 0..2
+  return (csum >> (12 - 4 * c)) & 15u;
+}
+
+template <int S, class V>
+__global__ void __launch_bounds__(kSmallBlock) wots_sign_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  constexpr int NW = Pr::NW;
+  const uint64_t per_msg = (uint64_t)Pr::d * Pr::wots_len;
+  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (uint64_t)a.count * per_msg) return;
+  const uint32_t msg = (uint32_t)(gid / per_msg);
+  const uint32_t rem = (uint32_t)(gid % per_msg);
+  const int layer = (int)(rem / Pr::wots_len);
+  const int chain = (int)(rem % Pr::wots_len);
+  const MsgPlan pl = a.plans[msg];
+  const KeyDev& K = a.keys[pl.key];
+  uint64_t tree;
+  uint32_t leaf;
+  layer_coords<S>(pl, layer, tree, leaf);
+  uint32_t mw[8];
+  const uint32_t* r = a.roots + ((size_t)msg * (Pr::d + 1) + layer) * 8;
+#pragma unroll
+  for (int j = 0; j < NW; j++) mw[j] = r[j];
+  const uint32_t digit = wots_digit<S>(mw, chain);
+  uint32_t mid[8], sks[NW];
+#pragma unroll
+  for (int j = 0; j < 8; j++) mid[j] = K.thash_mid[j];
+#pragma unroll
+  for (int j = 0; j < NW; j++) sks[j] = K.sk_seed[j];
+  Adrs wa = make_adrs((uint32_t)layer, tree, ADDR_WOTS, leaf, (uint32_t)chain, 0);
+  uint32_t st[8];
+  prf_reg<V, NW>(st, sks, wa);
+  uint32_t x[NW];
+#pragma unroll
+  for (int j = 0; j < NW; j++) x[j] = st[j];
+#pragma unroll 1
+  for (uint32_t s = 0; s < digit; s++) {
+    adrs_set_chain_hash(wa, (uint32_t)chain, s);
+    thash_reg<V, NW>(st, mid, wa, x);
+#pragma unroll
+    for (int j = 0; j < NW; j++) x[j] = st[j];
+  }
+  store_node<NW>(a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_ht + (size_t)layer * Pr::layer_bytes + chain * Pr::n,
+                 x);
+}
+
+// ---------------------------------------------------------------------------
+// keygen: root of the top subtree (layer d-1, tree 0) per key.  Thread =
+// (key, leaf); same leaf routine and shuffle reduction as TREE_Sign.
+// a.sk_bytes holds seed || 0^n per key (4n stride); a.keys the setup records.
+// ---------------------------------------------------------------------------
+template <int S, class V>
+__global__ void __launch_bounds__(kTreeBlock) keygen_root_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  constexpr int NW = Pr::NW;
+  __shared__ uint32_t tbuf[16 * kTreeBlock];
+  const uint64_t gid = (uint64_t)blockIdx.x * kTreeBlock + threadIdx.x;
+  const bool valid = gid < (uint64_t)a.nkeys * Pr::leaves;
+  const uint32_t key = valid ? (uint32_t)(gid / Pr::leaves) : 0u;
+  const uint32_t leaf = (uint32_t)(gid % Pr::leaves);
+  const uint32_t layer = Pr::d - 1;
+  uint32_t node[8];
+  const KeyDev& K = a.keys[key];
+  if (valid) wots_leaf<S, V>(K, layer, 0ull, leaf, &tbuf[threadIdx.x], kTreeBlock, node);
+#pragma unroll 1
+  for (int lvl = 1; lvl <= Pr::hp; lvl++) {
+    uint32_t other[NW];
+#pragma unroll
+    for (int j = 0; j < NW; j++) other[j] = __shfl_down_sync(0xffffffffu, node[j], 1u << (lvl - 1));
+    if (valid && (leaf & ((1u << lvl) - 1u)) == 0u) {
+      uint32_t m[2 * NW], mid[8];
+#pragma unroll
+      for (int j = 0; j < NW; j++) { m[j] = node[j]; m[NW + j] = other[j]; }
+#pragma unroll
+      for (int j = 0; j < 8; j++) mid[j] = K.thash_mid[j];
+      thash_reg<V, 2 * NW>(node, mid, make_adrs(layer, 0ull, ADDR_HASHTREE, 0, (uint32_t)lvl, leaf >> lvl), m);
+    }
+  }
+  if (valid && leaf == 0) {
+    uint8_t* sk = a.sk_out + (size_t)key * Pr::sk_bytes;
+    for (int j = 0; j < 3 * Pr::n; j++) sk[j] = a.sk_bytes[(size_t)key * Pr::sk_bytes + j];
+    store_node<NW>(sk + 3 * Pr::n, node);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Batched verification: one warp per message (sigcore.py:181-221,
+// fors_pk_from_sig oracle.py:149-178, wots_pk_from_sig wots.py:98-116,
+// compute_root oracle.py:66-95).  FORS trees and WOTS chains spread over the
+// lanes; the serial T_k / T_len / auth-path walks run on lane 0.
+// ---------------------------------------------------------------------------
+constexpr int kVerifyWarps = 4;
+
+template <int S>
+__device__ __forceinline__ void load_node(const uint8_t* p, uint32_t* x) {
+#pragma unroll
+  for (int j = 0; j < P<S>::NW; j++) x[j] = bswap32(*reinterpret_cast<const uint32_t*>(p + 4 * j));
+}
+
+// compute_root (oracle.py:66-95) for a node at leaf_idx within a forest offset
+template <int S, class V>
+__device__ __forceinline__ void walk_auth(uint32_t node[8], const uint32_t mid[8], Adrs a, uint32_t li, uint32_t off,
+                                          const uint8_t* auth, int height) {
+  constexpr int NW = P<S>::NW;
+#pragma unroll 1
+  for (int i = 0; i < height; i++) {
+    uint32_t sib[NW], m[2 * NW];
+    load_node<S>(auth + i * P<S>::n, sib);
+    const bool odd = li & 1u;
+#pragma unroll
+    for (int j = 0; j < NW; j++) {
+      m[j] = odd ? sib[j] : node[j];
+      m[NW + j] = odd ? node[j] : sib[j];
+    }
+    li >>= 1;
+    off >>= 1;
+    adrs_set_chain_hash(a, (uint32_t)(i + 1), li + off);
+    thash_reg<V, 2 * NW>(node, mid, a, m);
+  }
+}
+
+template <int S, class V>
+__global__ void __launch_bounds__(32 * kVerifyWarps) verify_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  constexpr int NW = Pr::NW;
+  __shared__ uint32_t s_ends[kVerifyWarps][Pr::wots_len > Pr::k ? Pr::wots_len * NW : Pr::k * NW];
+  __shared__ uint32_t s_col[kVerifyWarps][16];
+  __shared__ uint32_t s_root[kVerifyWarps][8];
+  __shared__ uint32_t s_mid[kVerifyWarps][8];
+  __shared__ uint64_t s_tree[kVerifyWarps];
+  __shared__ uint32_t s_leaf[kVerifyWarps];
+  __shared__ uint16_t s_idx[kVerifyWarps][Pr::k];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t i = blockIdx.x * kVerifyWarps + warp;
+  if (i >= a.count) return;  // whole warp exits together
+  const uint32_t key = a.key_idx ? a.key_idx[i] : 0u;
+  const uint8_t* pk = a.pks + (size_t)key * 2 * Pr::n;
+  const uint8_t* sig = a.vsigs + (size_t)i * Pr::sig_bytes;
+  uint32_t pk_seed[8], pk_root[8];
+  for (int j = 0; j < 8; j++) {
+    pk_seed[j] = j < NW ? load_be(pk + 4 * j) : 0u;
+    pk_root[j] = j < NW ? load_be(pk + Pr::n + 4 * j) : 0u;
+  }
+  if (lane == 0) {
+    uint32_t mid[8], W[16];
+    for (int j = 0; j < 8; j++) mid[j] = IVc(j);
+    for (int j = 0; j < 16; j++) W[j] = j < NW ? pk_seed[j] : 0u;
+    compress<V>(mid, W);
+    for (int j = 0; j < 8; j++) s_mid[warp][j] = mid[j];
+    // H_msg with R = sig[0:n] (hashes.py:175-191)
+    uint32_t R[8], dig0[8];
+    for (int j = 0; j < 8; j++) R[j] = j < NW ? load_be(sig + 4 * j) : 0u;
+    const uint8_t* msg = a.msgs + a.offs[i];
+    const uint64_t mlen = a.offs[i + 1] - a.offs[i];
+    ByteSha<V> hsh;
+    hsh.init_iv();
+    hsh.words(R, Pr::n);
+    hsh.words(pk_seed, Pr::n);
+    hsh.words(pk_root, Pr::n);
+    hsh.bytes(msg, mlen);
+    hsh.final(dig0);
+    uint8_t dg[64];
+    constexpr int nctr = (Pr::digest_bytes + 31) / 32;
+    for (int c = 0; c < nctr; c++) {
+      uint32_t o[8];
+      hsh.init_iv();
+      hsh.words(R, Pr::n);
+      hsh.words(pk_seed, Pr::n);
+      hsh.words(dig0, 32);
+      hsh.word((uint32_t)c);
+      hsh.final(o);
+      for (int j = 0; j < 32; j++) dg[32 * c + j] = (uint8_t)(o[j >> 2] >> (24 - 8 * (j & 3)));
+    }
+    uint64_t tree = 0;
+    for (int j = 0; j < Pr::tree_bytes; j++) tree = (tree << 8) | dg[Pr::fors_msg_bytes + j];
+    if (Pr::tree_bits < 64) tree &= (1ull << (Pr::tree_bits < 64 ? Pr::tree_bits : 63)) - 1ull;
+    uint32_t leaf = 0;
+    for (int j = 0; j < Pr::leaf_bytes; j++) leaf = (leaf << 8) | dg[Pr::fors_msg_bytes + Pr::tree_bytes + j];
+    leaf &= (1u << Pr::leaf_bits) - 1u;
+    s_tree[warp] = tree;
+    s_leaf[warp] = leaf;
+    int off = 0;
+    for (int g = 0; g < Pr::k; g++) {
+      uint32_t v = 0;
+      for (int j = 0; j < Pr::log_t; j++, off++) v |= (uint32_t)((dg[off >> 3] >> (off & 7)) & 1) << j;
+      s_idx[warp][g] = (uint16_t)v;
+    }
+  }
+  __syncwarp();
+  uint32_t mid[8];
+  for (int j = 0; j < 8; j++) mid[j] = s_mid[warp][j];
+  uint64_t tree = s_tree[warp];
+  uint32_t leaf_idx = s_leaf[warp];
+
+  // FORS public key from the signature
+  const uint8_t* fsig = sig + Pr::off_fors;
+  constexpr int tree_sig = (1 + Pr::log_t) * Pr::n;
+  for (int g = lane; g < Pr::k; g += 32) {
+    const uint32_t sel = s_idx[warp][g];
+    Adrs fa = make_adrs(0, tree, ADDR_FORS_TREE, leaf_idx, 0, (uint32_t)(g * Pr::t) + sel);
+    uint32_t sk[NW], node[8];
+    load_node<S>(fsig + g * tree_sig, sk);
+    thash_reg<V, NW>(node, mid, fa, sk);
+    walk_auth<S, V>(node, mid, fa, sel, (uint32_t)(g * Pr::t), fsig + g * tree_sig + Pr::n, Pr::log_t);
+    for (int j = 0; j < NW; j++) s_ends[warp][g * NW + j] = node[j];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    TStream<V> ts;
+    ts.begin(mid, make_adrs(0, tree, ADDR_FORS_ROOTS, leaf_idx, 0, 0), s_col[warp], 1);
+    for (int g = 0; g < Pr::k; g++) ts.template push_node<NW>(&s_ends[warp][g * NW]);
+    ts.finish(22u + (uint32_t)(Pr::k * Pr::n));
+    for (int j = 0; j < NW; j++) s_root[warp][j] = ts.st[j];
+  }
+  __syncwarp();
+
+  const uint8_t* ht = sig + Pr::off_ht;
+#pragma unroll 1
+  for (int layer = 0; layer < Pr::d; layer++) {
+    uint32_t root[8];
+    for (int j = 0; j < NW; j++) root[j] = s_root[warp][j];
+    const uint8_t* wsig = ht + (size_t)layer * Pr::layer_bytes;
+    for (int c = lane; c < Pr::wots_len; c += 32) {
+      const uint32_t digit = wots_digit<S>(root, c);
+      uint32_t x[8];
+      load_node<S>(wsig + c * Pr::n, x);
+      Adrs wa = make_adrs((uint32_t)layer, tree, ADDR_WOTS, leaf_idx, (uint32_t)c, 0);
+      for (uint32_t s = digit; s < (uint32_t)(Pr::w - 1); s++) {
+        adrs_set_chain_hash(wa, (uint32_t)c, s);
+        thash_reg<V, NW>(x, mid, wa, x);
+      }
+      for (int j = 0; j < NW; j++) s_ends[warp][c * NW + j] = x[j];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      TStream<V> ts;
+      ts.begin(mid, make_adrs((uint32_t)layer, tree, ADDR_WOTS_PK, leaf_idx, 0, 0), s_col[warp], 1);
+      for (int c = 0; c < Pr::wots_len; c++) ts.template push_node<NW>(&s_ends[warp][c * NW]);
+      ts.finish(22u + (uint32_t)(Pr::wots_len * Pr::n));
+      uint32_t node[8];
+      for (int j = 0; j < 8; j++) node[j] = ts.st[j];
+      walk_auth<S, V>(node, mid, make_adrs((uint32_t)layer, tree, ADDR_HASHTREE, 0, 0, 0), leaf_idx, 0,
+                      wsig + Pr::wots_sig_bytes, Pr::hp);
+      for (int j = 0; j < NW; j++) s_root[warp][j] = node[j];
+    }
+    __syncwarp();
+    leaf_idx = (uint32_t)(tree & (uint64_t)(Pr::leaves - 1));
+    tree = shr64(tree, Pr::hp);
+  }
+  if (lane == 0) {
+    bool eq = true;
+    for (int j = 0; j < NW; j++) eq = eq && (s_root[warp][j] == pk_root[j]);
+    a.ok[i] = eq ? 1 : 0;
+  }
+}
+
+}  // namespace hs

@@ -1,0 +1,267 @@
+"""Engine: one handle per B200, wrapping the C-ABI (include/herosign_b200.h).
+
+This is the stage-level replacement for the reference's signer objects
+(GraphSigner batchgraph.py:245-353 and the sign path sigcore.py:139-178):
+a batch of messages goes host -> device once, is signed by one CUDA-graph
+launch (msg_prep -> {FORS_Sign -> T_k} || TREE_Sign -> WOTS_Sign) and comes
+back as contiguous signature bytes.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _lib
+from .errors import HeroSignError, UsageError
+from .params import SET_INDEX, derive
+
+KERNELS = ("FORS_Sign", "TREE_Sign", "WOTS_Sign", "host")  # hs_set_config.variant order
+
+
+def _u8ptr(buf):
+    if buf is None:
+        return None
+    if isinstance(buf, (bytes,)):
+        return ctypes.cast(ctypes.c_char_p(buf), ctypes.c_void_p)
+    if isinstance(buf, np.ndarray):
+        return ctypes.c_void_p(buf.ctypes.data)
+    if isinstance(buf, (bytearray, memoryview)):
+        return ctypes.cast((ctypes.c_char * len(buf)).from_buffer(buf), ctypes.c_void_p)
+    if isinstance(buf, int):
+        return ctypes.c_void_p(buf)
+    raise UsageError(f"unsupported buffer type {type(buf).__name__}")
+
+
+def pack_messages(msgs: Sequence[bytes]) -> tuple[bytes, np.ndarray]:
+    offs = np.zeros(len(msgs) + 1, dtype=np.uint64)
+    if msgs:
+        np.cumsum([len(m) for m in msgs], out=offs[1:])
+    return b"".join(msgs), offs
+
+
+class Engine:
+    """Batched SPHINCS+ signing on one CUDA device."""
+
+    def __init__(self, device: int | None = None):
+        L = _lib.lib()
+        self.device = _lib.default_device() if device is None else int(device)
+        h = ctypes.c_void_p()
+        rc = L.hs_open(self.device, ctypes.byref(h))
+        if rc != _lib.HS_OK or not h.value:
+            raise HeroSignError(f"hs_open(device={self.device}) failed (rc={rc}): no usable CUDA device")
+        self._h = h
+        self._lock = threading.Lock()
+        self._keys: dict[str, bytes] = {}
+
+    # -- lifecycle -------------------------------------------------------
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.lib().hs_close(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown ordering
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int, what: str) -> None:
+        _lib.check(self._h, rc, what)
+
+    # -- device / config -------------------------------------------------
+    def device_info(self) -> dict:
+        v = [ctypes.c_int32() for _ in range(4)]
+        self._check(_lib.lib().hs_device_info(self._h, *[ctypes.byref(x) for x in v]), "hs_device_info")
+        return {"sm_count": v[0].value, "smem_optin": v[1].value, "cc": (v[2].value, v[3].value)}
+
+    def config(self, set_id: str) -> dict:
+        c = _lib.SetConfig()
+        self._check(_lib.lib().hs_config_get(self._h, SET_INDEX[set_id], ctypes.byref(c)), "hs_config_get")
+        return {
+            "fors_trees_per_set": c.fors_trees_per_set,
+            "fors_sets_fused": c.fors_sets_fused,
+            "fors_relax": bool(c.fors_relax),
+            "variant": {k: int(c.variant[i]) for i, k in enumerate(KERNELS)},
+            "use_graph": bool(c.use_graph),
+            "chunk": c.chunk,
+        }
+
+    def set_config(self, set_id: str, **kw) -> dict:
+        cur = self.config(set_id)
+        variant = dict(cur["variant"])
+        variant.update(kw.pop("variant", {}) or {})
+        cur.update(kw)
+        c = _lib.SetConfig()
+        c.fors_trees_per_set = int(cur["fors_trees_per_set"])
+        c.fors_sets_fused = int(cur["fors_sets_fused"])
+        c.fors_relax = int(bool(cur["fors_relax"]))
+        for i, k in enumerate(KERNELS):
+            c.variant[i] = int(variant[k])
+        c.use_graph = int(bool(cur["use_graph"]))
+        c.chunk = int(cur["chunk"])
+        self._check(_lib.lib().hs_config_set(self._h, SET_INDEX[set_id], ctypes.byref(c)), "hs_config_set")
+        return self.config(set_id)
+
+    @staticmethod
+    def fors_smem_bytes(set_id: str, trees_per_set: int, sets_fused: int, relax: bool) -> int:
+        return int(_lib.lib().hs_fors_smem_bytes(SET_INDEX[set_id], trees_per_set, sets_fused, int(relax)))
+
+    # -- keys ------------------------------------------------------------
+    def upload_keys(self, set_id: str, sks: bytes | Iterable[bytes]) -> int:
+        p = derive(set_id)
+        blob = sks if isinstance(sks, (bytes, bytearray)) else b"".join(sks)
+        blob = bytes(blob)
+        if not blob or len(blob) % p.sk_bytes:
+            raise UsageError(f"key table must be a non-empty multiple of {p.sk_bytes} bytes")
+        if self._keys.get(set_id) == blob:
+            return len(blob) // p.sk_bytes
+        with self._lock:
+            self._check(_lib.lib().hs_keys_upload(self._h, p.index, _u8ptr(blob), len(blob) // p.sk_bytes),
+                        "hs_keys_upload")
+            self._keys[set_id] = blob
+        return len(blob) // p.sk_bytes
+
+    def keygen_batch(self, set_id: str, seeds: Sequence[bytes]) -> list[bytes]:
+        p = derive(set_id)
+        for s in seeds:
+            if len(s) != 3 * p.n:
+                raise UsageError(f"seed must be {3 * p.n} bytes, got {len(s)}")
+        if not seeds:
+            return []
+        blob = b"".join(seeds)
+        out = bytearray(len(seeds) * p.sk_bytes)
+        with self._lock:
+            self._check(_lib.lib().hs_keygen_batch(self._h, p.index, _u8ptr(blob), len(seeds), _u8ptr(out)),
+                        "hs_keygen_batch")
+        return [bytes(out[i * p.sk_bytes:(i + 1) * p.sk_bytes]) for i in range(len(seeds))]
+
+    # -- signing ---------------------------------------------------------
+    def sign_into(self, set_id: str, blob, offs: np.ndarray, count: int, out, key_idx: np.ndarray | None = None,
+                  opt_rand=None) -> None:
+        """Zero-copy batch sign: inputs/outputs are caller buffers (pinned ones avoid staging)."""
+        p = derive(set_id)
+        with self._lock:
+            self._check(
+                _lib.lib().hs_sign_batch(self._h, p.index, _u8ptr(blob), _u8ptr(offs),
+                                         _u8ptr(key_idx) if key_idx is not None else None, _u8ptr(opt_rand),
+                                         count, _u8ptr(out)),
+                "hs_sign_batch")
+
+    def sign_batch(self, set_id: str, msgs: Sequence[bytes], key_idx: Sequence[int] | None = None,
+                   opt_rand: Sequence[bytes] | bytes | None = None) -> list[bytes]:
+        p = derive(set_id)
+        if set_id not in self._keys:
+            raise UsageError("no keys uploaded for this parameter set")
+        count = len(msgs)
+        if count == 0:
+            return []
+        blob, offs = pack_messages(msgs)
+        kidx = None
+        if key_idx is not None:
+            kidx = np.ascontiguousarray(key_idx, dtype=np.uint32)
+            if kidx.shape != (count,):
+                raise UsageError("key_idx must hold one entry per message")
+        orand = None
+        if opt_rand is not None:
+            orand = opt_rand if isinstance(opt_rand, (bytes, bytearray)) else b"".join(opt_rand)
+            if len(orand) != count * p.n:
+                raise UsageError(f"opt_rand must be {p.n} bytes per message")
+            orand = bytes(orand)
+        out = bytearray(count * p.sig_bytes)
+        self.sign_into(set_id, blob, offs, count, out, kidx, orand)
+        sb = p.sig_bytes
+        return [bytes(out[i * sb:(i + 1) * sb]) for i in range(count)]
+
+    def verify_batch(self, set_id: str, pks: Sequence[bytes] | bytes, msgs: Sequence[bytes], sigs: Sequence[bytes],
+                     key_idx: Sequence[int] | None = None) -> list[bool]:
+        p = derive(set_id)
+        count = len(msgs)
+        if len(sigs) != count:
+            raise UsageError("one signature per message required")
+        if count == 0:
+            return []
+        pkb = pks if isinstance(pks, (bytes, bytearray)) else b"".join(pks)
+        if not pkb or len(pkb) % p.pk_bytes:
+            raise UsageError(f"public keys must be a multiple of {p.pk_bytes} bytes")
+        ok = np.zeros(count, dtype=np.uint8)
+        good = [len(s) == p.sig_bytes for s in sigs]
+        sigblob = b"".join(s if g else bytes(p.sig_bytes) for s, g in zip(sigs, good))
+        blob, offs = pack_messages(msgs)
+        kidx = None if key_idx is None else np.ascontiguousarray(key_idx, dtype=np.uint32)
+        with self._lock:
+            self._check(_lib.lib().hs_verify_batch(self._h, p.index, _u8ptr(bytes(pkb)), len(pkb) // p.pk_bytes,
+                                                   _u8ptr(blob), _u8ptr(offs), _u8ptr(kidx), _u8ptr(sigblob),
+                                                   count, _u8ptr(ok)),
+                        "hs_verify_batch")
+        return [bool(o) and g for o, g in zip(ok.tolist(), good)]
+
+    # -- device-resident stages (bench / graph signer) ---------------------
+    def stage(self, set_id: str, blob, offs: np.ndarray, count: int, key_idx=None, opt_rand=None) -> None:
+        p = derive(set_id)
+        self._check(_lib.lib().hs_stage(self._h, p.index, _u8ptr(blob), _u8ptr(offs), _u8ptr(key_idx),
+                                        _u8ptr(opt_rand), count), "hs_stage")
+
+    def run(self, set_id: str, count: int, mode: int = 0) -> None:
+        self._check(_lib.lib().hs_run(self._h, SET_INDEX[set_id], count, mode), "hs_run")
+
+    def sync(self) -> None:
+        self._check(_lib.lib().hs_sync(self._h), "hs_sync")
+
+    def fetch(self, set_id: str, first: int, count: int, out) -> None:
+        self._check(_lib.lib().hs_fetch(self._h, SET_INDEX[set_id], first, count, _u8ptr(out)), "hs_fetch")
+
+    def timings(self) -> dict:
+        ms = (ctypes.c_float * 5)()
+        n = _lib.lib().hs_timings(self._h, ms, 5)
+        if n < 0:
+            self._check(n, "hs_timings")
+        names = ("batch", "msg_prep", "FORS_Sign", "TREE_Sign", "WOTS_Sign")
+        return {names[i]: float(ms[i]) for i in range(max(n, 0))}
+
+    @property
+    def launch_count(self) -> int:
+        return int(_lib.lib().hs_launch_count(self._h))
+
+
+class PinnedBuffer:
+    """Page-locked host buffer (cudaMallocHost) exposed as a writable memoryview."""
+
+    def __init__(self, nbytes: int):
+        self.nbytes = int(nbytes)
+        ptr = _lib.lib().hs_host_alloc(max(self.nbytes, 1))
+        if not ptr:
+            raise HeroSignError(f"cudaMallocHost({nbytes}) failed")
+        self.ptr = int(ptr)
+        self.view = (ctypes.c_char * max(self.nbytes, 1)).from_address(self.ptr)
+
+    def array(self, dtype=np.uint8) -> np.ndarray:
+        return np.frombuffer(self.view, dtype=dtype)
+
+    def free(self) -> None:
+        if self.ptr:
+            _lib.lib().hs_host_free(ctypes.c_void_p(self.ptr))
+            self.ptr = 0
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+_ENGINES: dict[int, Engine] = {}
+_ENGINES_LOCK = threading.Lock()
+
+
+def get_engine(device: int | None = None) -> Engine:
+    """Process-wide engine for a device (default: $HEROSIGN_DEVICE / $LOCAL_RANK / 0)."""
+    dev = _lib.default_device() if device is None else int(device)
+    with _ENGINES_LOCK:
+        eng = _ENGINES.get(dev)
+        if eng is None:
+            eng = _ENGINES[dev] = Engine(dev)
+        return eng

@@ -1,0 +1,159 @@
+"""GPU parity: the CUDA engine (through the C-ABI) against the reference's
+golden fixtures and the C oracle.  Bit-exact: every signature byte must match."""
+
+from __future__ import annotations
+
+import hashlib
+import random
+
+import pytest
+
+from conftest import GOLDEN_DIR, SETS
+
+import paper_2512_23969_b200 as hs
+from paper_2512_23969_b200.params import derive
+
+pytestmark = pytest.mark.gpu
+H = bytes.fromhex
+
+
+@pytest.fixture(scope="module")
+def eng():
+    return hs.get_engine()
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_keygen_golden(eng, golden, set_id):
+    g = golden["sets"][set_id]["keygen"]
+    assert eng.keygen_batch(set_id, [H(g["seed"])])[0].hex() == g["sk"]
+    sk = hs.keygen(set_id, H(g["seed"]))
+    assert sk.to_bytes().hex() == g["sk"]
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_sign_golden(eng, golden, set_id):
+    g = golden["sets"][set_id]
+    p = derive(set_id)
+    for case in g["sign"]:
+        sk = hs.SecretKey.from_bytes(H(case["sk"]), p)
+        opt = H(case["opt_rand"]) if case["opt_rand"] else None
+        sig = hs.sign(H(case["msg"]), sk, p, opt_rand=opt)
+        if case["tag"] == "zero":
+            ref = (GOLDEN_DIR / f"sig_{set_id}_zero.bin").read_bytes()
+            if sig != ref:
+                bad = [i for i in range(len(ref)) if sig[i] != ref[i]]
+                regions = hs.signature_regions(p)
+                where = sorted({name for name, (lo, hi) in regions.items() for b in bad[:200] if lo <= b < hi})
+                pytest.fail(f"{len(bad)} bytes differ; first at {bad[0]}; regions {where[:8]}")
+        assert hashlib.sha256(sig).hexdigest() == case["sig_sha256"], case["tag"]
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_bench_recipe_golden(eng, golden, set_id):
+    g = golden["sets"][set_id]["bench_recipe"]
+    rng = random.Random(2512_23969)
+    p = derive(set_id)
+    rng.randbytes(3 * p.n)
+    msgs = [rng.randbytes(32) for _ in range(len(g["sig_sha256"]))]
+    sigs = hs.sign_batch(msgs, hs.SecretKey.from_bytes(H(g["sk"]), p), p)
+    assert [hashlib.sha256(s).hexdigest() for s in sigs] == g["sig_sha256"]
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_mixed_batch_vs_oracle(eng, oracle_mod, set_id):
+    """Ragged messages (0..300 B), several keys, explicit and default opt_rand."""
+    p = derive(set_id)
+    rng = random.Random(7 + p.n)
+    seeds = [rng.randbytes(3 * p.n) for _ in range(3)]
+    sks = [oracle_mod.keygen(set_id, s) for s in seeds]
+    count = 40
+    msgs = [rng.randbytes(rng.choice([0, 1, 3, 31, 32, 33, 55, 56, 64, 65, 119, 300])) for _ in range(count)]
+    kidx = [rng.randrange(3) for _ in range(count)]
+    opts = [rng.randbytes(p.n) if i % 3 == 0 else None for i in range(count)]
+    keys = [hs.SecretKey.from_bytes(s, p) for s in sks]
+    sigs = hs.sign_batch(msgs, keys, p, key_idx=kidx, opt_rand=opts)
+    for i in range(count):
+        ref = oracle_mod.sign(set_id, sks[kidx[i]], msgs[i], opts[i])
+        assert sigs[i] == ref, i
+
+
+@pytest.mark.parametrize("set_id", SETS)
+@pytest.mark.parametrize("variant", [0, 1])
+def test_layouts_and_variants(eng, oracle_mod, set_id, variant):
+    """Every FORS fusion layout / relax mode and both SHA-256 paths give identical bytes."""
+    p = derive(set_id)
+    rng = random.Random(99)
+    sk = oracle_mod.keygen(set_id, rng.randbytes(3 * p.n))
+    msgs = [rng.randbytes(32) for _ in range(6)]
+    ref = [oracle_mod.sign(set_id, sk, m) for m in msgs]
+    eng.upload_keys(set_id, sk)
+    base = eng.config(set_id)
+    layouts = {"128f": [(1, 1, 0), (11, 3, 0), (2, 5, 1), (16, 2, 1)],
+               "192f": [(1, 1, 0), (3, 3, 0), (4, 2, 1), (2, 5, 1)],
+               "256f": [(1, 1, 0), (2, 2, 1), (1, 5, 1), (4, 1, 1)]}[set_id]
+    try:
+        for nt, f, rx in layouts:
+            eng.set_config(set_id, fors_trees_per_set=nt, fors_sets_fused=f, fors_relax=bool(rx),
+                           variant={k: variant for k in ("FORS_Sign", "TREE_Sign", "WOTS_Sign", "host")})
+            assert eng.sign_batch(set_id, msgs) == ref, (nt, f, rx)
+    finally:
+        eng.set_config(set_id, **base)
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_verify_gpu(eng, golden, set_id):
+    p = derive(set_id)
+    g = golden["sets"][set_id]
+    sk = H(g["keygen"]["sk"])
+    pk = hs.PublicKey.from_bytes(sk[2 * p.n:], p)
+    sig = (GOLDEN_DIR / f"sig_{set_id}_zero.bin").read_bytes()
+    assert hs.verify(bytes(32), sig, pk, p)
+    assert not hs.verify(bytes(31) + b"\x01", sig, pk, p)
+    assert not hs.verify(bytes(32), sig[:-1], pk, p)
+    rng = random.Random(5)
+    bad = []
+    for _ in range(24):
+        b = bytearray(sig)
+        b[rng.randrange(len(b))] ^= 1 << rng.randrange(8)
+        bad.append(bytes(b))
+    res = hs.verify_batch([bytes(32)] * len(bad), bad, pk, p)
+    assert not any(res)
+
+
+def test_verify_exhaustive_corruption_128f(eng, golden):
+    """every single-byte corruption of a 128f signature fails."""
+    p = derive("128f")
+    sk = H(golden["sets"]["128f"]["keygen"]["sk"])
+    pk = hs.PublicKey.from_bytes(sk[32:], p)
+    sig = (GOLDEN_DIR / "sig_128f_zero.bin").read_bytes()
+    bad = []
+    for pos in range(len(sig)):
+        b = bytearray(sig)
+        b[pos] ^= 0xFF
+        bad.append(bytes(b))
+    res = hs.verify_batch([bytes(32)] * len(bad), bad, pk, p)
+    assert not any(res)
+
+
+def test_errors(eng):
+    p = derive("128f")
+    with pytest.raises(hs.UsageError):
+        hs.sign(b"x", hs.SecretKey.from_bytes(bytes(64), p), p, opt_rand=b"short")
+    sk = hs.SecretKey.from_bytes(bytes(64), p)
+    with pytest.raises(hs.UsageError):
+        hs.sign_batch([b"a", b"b"], [sk], p, key_idx=[0, 3])
+    with pytest.raises(hs.ConfigError):
+        eng.set_config("128f", fors_trees_per_set=17, fors_sets_fused=1)  # 1088 lanes
+
+
+def test_config2_full_batch_128f(eng, oracle_mod):
+    """BASELINE config 2: 4096 messages, one key, every signature checked vs the CPU oracle."""
+    p = derive("128f")
+    rng = random.Random(2512_23969)
+    sk = oracle_mod.keygen("128f", rng.randbytes(3 * p.n))
+    msgs = [rng.randbytes(32) for _ in range(4096)]
+    eng.upload_keys("128f", sk)
+    sigs = eng.sign_batch("128f", msgs)
+    ref, _ = oracle_mod.sign_many("128f", sk, None, msgs)
+    assert sigs == ref
+    assert all(eng.verify_batch("128f", sk[32:], msgs, sigs))
