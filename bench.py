@@ -1,0 +1,367 @@
+"""Benchmark: batched SPHINCS+ signing throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--set 128f] [--count 4096]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference ...      # the CPU reference arm
+
+Workload (BASELINE.json configs[1]): SPHINCS+-128f, 4096 synthetic 32-byte
+messages per GPU, one key, rng = random.Random(2512_23969).
+A step signs the whole batch: one CUDA-graph launch of msg_prep ->
+{FORS_Sign -> T_k} || TREE_Sign -> WOTS_Sign.  Weak scaling: each rank signs
+its own 4096-message shard; no collective is on the signing path (the only
+torch.distributed traffic is the barrier and the max-over-ranks of times).
+
+value  : whole-job signatures/s with inputs resident in HBM (device-timed,
+         CUDA events per step on the launching stream, L2 flushed between
+         steps by rewriting a 256 MiB buffer outside the events).
+e2e    : the same metric through the public API (hs_sign_batch via
+         Engine.sign_into) from pinned host buffers: H2D of the messages,
+         signing, D2H of every signature, each step; host wall clock.
+roofline: TREE_Sign (the dominant kernel, ~89% of 128f work) against the
+         B200 integer-issue roofline N_SM * f_max * 128 / 1384 compressions/s
+         (SURVEY.md s.8(d)); its duration is taken with CUDA events around the
+         kernel in a serialised run (hs_run mode 1) inside this process.
+cpu_baseline: the C restatement of the reference signer (oracle/, a "port"),
+         all host threads, a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+SEED = 2512_23969
+OPS_PER_COMPRESSION = 1384     # canonical integer ops of one SHA-256 compression
+ISSUE_PER_CLK_PER_SM = 128     # 4 SMSPs x 32 lanes
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--set", dest="set_id", default="128f", choices=["128f", "192f", "256f"])
+    ap.add_argument("--count", type=int, default=4096, help="messages per GPU per step")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample length")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--check", type=int, default=16, help="signatures checked vs the oracle after timing")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def init_dist(world: int):
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+
+    dist.init_process_group(backend="gloo")
+    return dist
+
+
+def max_over_ranks(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def workload(set_id: str, count: int, rank: int):
+    """BASELINE.md s.3 recipe; rank r's shard continues the same RNG stream."""
+    from paper_2512_23969_b200.params import derive
+
+    p = derive(set_id)
+    rng = random.Random(SEED)
+    seed = rng.randbytes(3 * p.n)
+    for _ in range(rank * count):
+        rng.randbytes(32)
+    msgs = [rng.randbytes(32) for _ in range(count)]
+    return p, seed, msgs
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.out = ""
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out = ""
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                clk, cmax = float(f[1]), float(f[2])
+            except ValueError:
+                continue
+            mx = max(mx, cmax)
+            sm.append(clk)
+            for name, val in zip(names, f[5:9]):
+                if val.lower() in ("active", "1"):
+                    reasons.add(name)
+        loaded = [c for c in sm if c > 0.5 * mx] if mx else sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_sign_rate(set_id: str, sk: bytes, msgs: list[bytes], seconds: float, threads: int):
+    """Oracle port (C, all host threads) on a bounded sample; returns (sig/s, sample size, wall s)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle  # CPU baseline leg only
+
+    oracle.build()
+    probe = msgs[: max(threads, 8)]
+    t0 = time.perf_counter()
+    oracle.sign_many(set_id, sk, None, probe, threads=threads)
+    dt = time.perf_counter() - t0
+    rate0 = len(probe) / max(dt, 1e-9)
+    n = int(min(len(msgs) * 4, max(threads * 2, rate0 * seconds)))
+    sample = [msgs[i % len(msgs)] for i in range(n)]
+    t0 = time.perf_counter()
+    oracle.sign_many(set_id, sk, None, sample, threads=threads)
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2512_23969_b200.params import derive
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle  # reference arm: the CPU restatement of the reference signer
+
+    oracle.build()
+    p, seed, msgs = workload(args.set_id, args.count, 0)
+    sk = oracle.keygen(args.set_id, seed)
+    threads = os.cpu_count() or 1
+    per_step = max(threads, int(threads * 2))
+    rate_probe, _, _ = cpu_sign_rate(args.set_id, sk, msgs, 1.0, threads)
+    per_step = int(max(threads, min(args.count, rate_probe * max(1.0, 60.0 / max(1, args.steps + args.warmup)))))
+    for _ in range(args.warmup):
+        oracle.sign_many(args.set_id, sk, None, msgs[:threads], threads=threads)
+    times = []
+    for s in range(args.steps):
+        batch = [msgs[(s * per_step + i) % len(msgs)] for i in range(per_step)]
+        t0 = time.perf_counter()
+        oracle.sign_many(args.set_id, sk, None, batch, threads=threads)
+        times.append(time.perf_counter() - t0)
+    value = per_step * len(times) / sum(times)
+    line = {
+        "impl": "reference", "metric": f"signatures/sec SPHINCS+-{args.set_id}", "value": round(value, 3),
+        "unit": "sig/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * statistics.mean(times), 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"SPHINCS+-{args.set_id} sign, {args.count} x 32-byte msgs, 1 key (per-step sample "
+                               f"of {per_step} msgs)", "set": args.set_id},
+        "cpu_baseline": {"value": round(value, 3), "unit": "sig/s", "cores": threads, "kind": "port",
+                         "sample": f"{per_step} signatures per step x {args.steps} steps, C oracle "
+                                   f"(oracle/hs_oracle.c, SHA-NI={oracle.shani_active()})"},
+        "e2e": {"value": round(value, 3), "unit": "sig/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    rank, world, local = dist_env()
+    dist = init_dist(world)
+    import numpy as np
+
+    import paper_2512_23969_b200 as hs
+    from paper_2512_23969_b200.engine import PinnedBuffer, pack_messages
+
+    eng = hs.get_engine(local)
+    info = eng.device_info()
+    p, seed, msgs = workload(args.set_id, args.count, rank)
+    sk = eng.keygen_batch(args.set_id, [seed])[0]
+    eng.upload_keys(args.set_id, sk)
+    blob, offs = pack_messages(msgs)
+    count = len(msgs)
+
+    # ---- value: inputs resident in HBM, device-timed graph launches ----
+    eng.stage(args.set_id, blob, offs, count)
+    flush = 256 << 20
+    eng.bench_run(args.set_id, count, max(1, args.warmup), 0, flush)
+    launches0 = eng.launch_count
+    barrier(dist)
+    with ClockSampler(local) as clocks:
+        step_ms = eng.bench_run(args.set_id, count, args.steps, 0, flush)
+    launches = eng.launch_count - launches0
+    barrier(dist)
+    dev_s = max_over_ranks(dist, sum(step_ms) / 1e3)
+    value = world * count * args.steps / dev_s
+    graph_ms = eng.timings()
+
+    # ---- per-kernel roofline (serialised run, CUDA events around each kernel) ----
+    ser = [eng.bench_run(args.set_id, count, 1, 1, flush) for _ in range(3)]
+    kt = [eng.timings() for _ in range(1)]
+    tree_ms = []
+    for _ in range(3):
+        eng.bench_run(args.set_id, count, 1, 1, flush)
+        tree_ms.append(eng.timings()["TREE_Sign"])
+    tree_ms_avg = statistics.mean(tree_ms)
+    work = hs.compressions_per_signature(p, 32)
+    tree_comps = work["TREE_Sign"] * count
+    achieved = tree_comps / (tree_ms_avg / 1e3)
+    sm_max = clocks.summary().get("sm_max_mhz") or 1965.0
+    peak = info["sm_count"] * sm_max * 1e6 * ISSUE_PER_CLK_PER_SM / OPS_PER_COMPRESSION
+    traffic = None
+    tpath = ROOT / "profiles" / "tree_traffic.json"
+    if tpath.exists():
+        try:
+            traffic = json.loads(tpath.read_text()).get(args.set_id, {}).get("bytes_per_launch_per_msg")
+            traffic = traffic * count if traffic is not None else None
+        except (ValueError, AttributeError):
+            traffic = None
+
+    # ---- e2e: public API, pinned host buffers, H2D + sign + D2H every step ----
+    h_blob = PinnedBuffer(max(len(blob), 1))
+    h_blob.array()[: len(blob)] = np.frombuffer(blob, dtype=np.uint8)
+    h_offs = PinnedBuffer(offs.nbytes)
+    h_offs.array(np.uint64)[:] = offs
+    h_out = PinnedBuffer(count * p.sig_bytes)
+    for _ in range(max(1, args.warmup)):
+        eng.sign_into(args.set_id, h_blob.ptr, h_offs.array(np.uint64), count, h_out.ptr)
+    barrier(dist)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        eng.sign_into(args.set_id, h_blob.ptr, h_offs.array(np.uint64), count, h_out.ptr)
+    e2e_s = max_over_ranks(dist, time.perf_counter() - t0)
+    e2e = world * count * args.steps / e2e_s
+    sigs_out = bytes(h_out.view[: count * p.sig_bytes])
+
+    # ---- correctness spot check of this step's output vs the oracle ----
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle  # checker
+
+    oracle.build()
+    chk = list(range(0, count, max(1, count // max(1, args.check))))[: args.check]
+    ref, _ = oracle.sign_many(args.set_id, sk, None, [msgs[i] for i in chk])
+    ok = all(sigs_out[i * p.sig_bytes:(i + 1) * p.sig_bytes] == r for i, r in zip(chk, ref))
+    ok_all = max_over_ranks(dist, 0.0 if ok else 1.0) == 0.0
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, n, dt = cpu_sign_rate(args.set_id, sk, msgs, args.cpu_seconds, threads)
+        cpu = {"value": round(rate, 3), "unit": "sig/s", "cores": threads, "kind": "port",
+               "sample": f"{n} of the same {args.set_id} messages in {dt:.1f}s, C oracle (oracle/hs_oracle.c, "
+                         f"SHA-NI={oracle.shani_active()})"}
+
+    if rank == 0:
+        clk = clocks.summary()
+        line = {
+            "metric": f"signatures/sec SPHINCS+-{args.set_id}",
+            "value": round(value, 1),
+            "unit": "sig/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(1e3 * dev_s / args.steps, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "u32",
+            "data": "synthetic",
+            "config": {
+                "workload": f"SPHINCS+-{args.set_id} batched sign, {count} x 32-byte msgs per GPU, 1 key "
+                            f"(BASELINE configs[1])",
+                "set": args.set_id, "messages_per_gpu": count, "global_batch": world * count,
+                "parallelism": f"message-shard x{world}", "l2": "flushed between steps (256 MiB rewrite)",
+                "fors_layout": {k: v for k, v in eng.config(args.set_id).items() if k.startswith("fors")},
+                "variant": eng.config(args.set_id)["variant"],
+            },
+            "e2e": {"value": round(e2e, 1), "unit": "sig/s",
+                    "h2d_bytes_per_step": int(len(blob) + offs.nbytes),
+                    "d2h_bytes_per_step": int(count * p.sig_bytes)},
+            "gpu_launches": int(launches),
+            "roofline": {
+                "bound": "int-issue",
+                "kernel": "TREE_Sign",
+                "achieved": round(achieved / 1e9, 3),
+                "peak": round(peak / 1e9, 3),
+                "unit": "Gcompressions/s",
+                "frac": round(achieved / peak, 4),
+                "traffic": traffic,
+                "work_per_launch": f"{work['TREE_Sign']} compressions/msg x {count} msgs",
+                "kernel_ms": round(tree_ms_avg, 3),
+                "peak_basis": f"{info['sm_count']} SMs x {sm_max:.0f} MHz x 128 / 1384",
+            },
+            "kernel_ms_graph": {k: round(v, 3) for k, v in graph_ms.items()},
+            "kernel_ms_serial": {k: round(v, 3) for k, v in kt[0].items()},
+            "hbm_sig_writeout_gbs": round(count * p.sig_bytes / (statistics.mean(step_ms) / 1e3) / 1e9, 3),
+            "compressions_per_sig": work["total"],
+            "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
+            "parity_spot_check": {"checked": len(chk), "ok": ok_all},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    for b in (h_blob, h_offs, h_out):
+        b.free()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -121,6 +121,13 @@ HS_API int hs_fetch(hs_t *h, int set, uint32_t first, uint32_t count, uint8_t *s
  * [4] WOTS_Sign.  Returns the number of values written. */
 HS_API int hs_timings(hs_t *h, float *ms, int cap);
 
+/* Benchmark loop over the staged batch: `steps` runs (mode as hs_run), each
+ * bracketed by CUDA events on the launching stream; when flush_bytes > 0 a
+ * device buffer of that size is rewritten between steps (outside the events)
+ * to evict L2.  step_ms[steps] receives the per-step device times. */
+HS_API int hs_bench_run(hs_t *h, int set, uint32_t count, int32_t steps, int mode, uint64_t flush_bytes,
+                        float *step_ms);
+
 /* Kernel launches issued by this handle since open (for bench accounting). */
 HS_API int64_t hs_launch_count(hs_t *h);
 

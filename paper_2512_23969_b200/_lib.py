@@ -28,7 +28,7 @@ HS_E_CUDA = -10
 EXPORTS = (
     "hs_open", "hs_close", "hs_last_error", "hs_device_info", "hs_params", "hs_config_get", "hs_config_set",
     "hs_fors_smem_bytes", "hs_keys_upload", "hs_keygen_batch", "hs_sign_batch", "hs_verify_batch",
-    "hs_stage", "hs_run", "hs_sync", "hs_fetch", "hs_timings", "hs_launch_count", "hs_host_alloc",
+    "hs_stage", "hs_run", "hs_sync", "hs_fetch", "hs_timings", "hs_bench_run", "hs_launch_count", "hs_host_alloc",
     "hs_host_free",
 )
 
@@ -84,6 +84,8 @@ def lib() -> ctypes.CDLL:
         "hs_sync": (ctypes.c_int, [vp]),
         "hs_fetch": (ctypes.c_int, [vp, ctypes.c_int, u32, u32, u8p]),
         "hs_timings": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int]),
+        "hs_bench_run": (ctypes.c_int, [vp, ctypes.c_int, u32, i32, ctypes.c_int, ctypes.c_uint64,
+                                        ctypes.POINTER(ctypes.c_float)]),
         "hs_launch_count": (i64, [vp]),
         "hs_host_alloc": (vp, [ctypes.c_size_t]),
         "hs_host_free": (None, [vp]),

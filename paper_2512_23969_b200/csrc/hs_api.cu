@@ -140,6 +140,8 @@ struct hs_ctx {
   int last_set = -1;
   int last_mode = 0;
   int sm_count = 0, smem_optin = 0, cc_major = 0, cc_minor = 0;
+  void* flush = nullptr;
+  size_t flush_cap = 0;
 };
 
 namespace {
@@ -395,6 +397,7 @@ void hs_close(hs_t* h) {
     cudaFree(h->sets[s].keys);
     cudaFree(h->sets[s].sk_raw);
   }
+  if (h->flush) cudaFree(h->flush);
   for (auto& ev : h->ev) cudaEventDestroy(ev);
   cudaEventDestroy(h->fork);
   cudaEventDestroy(h->join);
@@ -636,6 +639,37 @@ int hs_timings(hs_t* h, float* ms, int cap) {
   int m = std::min(cap, 5);
   for (int i = 0; i < m; i++) ms[i] = v[i];
   return m;
+}
+
+int hs_bench_run(hs_t* h, int set, uint32_t count, int32_t steps, int mode, uint64_t flush_bytes, float* step_ms) {
+  if (!h || !valid_set(set) || steps < 1 || !step_ms) return fail(h, HS_E_USAGE, "bad arguments");
+  if (count == 0 || count > h->sets[set].staged) return fail(h, HS_E_USAGE, "count exceeds the staged batch");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  if (flush_bytes && flush_bytes > h->flush_cap) {
+    if (h->flush) cudaFree(h->flush);
+    h->flush = nullptr;
+    h->flush_cap = 0;
+    CUDA_TRY(h, cudaMalloc(&h->flush, flush_bytes));
+    h->flush_cap = flush_bytes;
+  }
+  std::vector<cudaEvent_t> ev(2 * (size_t)steps);
+  for (auto& e : ev) CUDA_TRY(h, cudaEventCreate(&e));
+  int rc = HS_OK;
+  for (int i = 0; i < steps && rc == HS_OK; i++) {
+    if (flush_bytes) {
+      cudaError_t e = cudaMemsetAsync(h->flush, i & 0xFF, flush_bytes, h->s0);
+      if (e != cudaSuccess) rc = fail(h, HS_E_CUDA, "flush: %s", cudaGetErrorString(e));
+    }
+    if (rc == HS_OK) cudaEventRecord(ev[2 * i], h->s0);
+    if (rc == HS_OK) rc = run_batch(h, set, count, mode);
+    if (rc == HS_OK) cudaEventRecord(ev[2 * i + 1], h->s0);
+  }
+  cudaError_t se = cudaStreamSynchronize(h->s0);
+  if (rc == HS_OK && se != cudaSuccess) rc = fail(h, HS_E_CUDA, "bench: %s", cudaGetErrorString(se));
+  if (rc == HS_OK)
+    for (int i = 0; i < steps; i++) cudaEventElapsedTime(&step_ms[i], ev[2 * i], ev[2 * i + 1]);
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
 }
 
 int64_t hs_launch_count(hs_t* h) { return h ? h->launches : -1; }

@@ -222,6 +222,13 @@ class Engine:
         names = ("batch", "msg_prep", "FORS_Sign", "TREE_Sign", "WOTS_Sign")
         return {names[i]: float(ms[i]) for i in range(max(n, 0))}
 
+    def bench_run(self, set_id: str, count: int, steps: int, mode: int = 0, flush_bytes: int = 0) -> list[float]:
+        """Per-step device ms of `steps` runs over the staged batch (CUDA events, launching stream)."""
+        ms = (ctypes.c_float * steps)()
+        self._check(_lib.lib().hs_bench_run(self._h, SET_INDEX[set_id], count, steps, mode, flush_bytes, ms),
+                    "hs_bench_run")
+        return [float(x) for x in ms]
+
     @property
     def launch_count(self) -> int:
         return int(_lib.lib().hs_launch_count(self._h))
