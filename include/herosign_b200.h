@@ -64,6 +64,9 @@ typedef struct {
                                  [3] message preparation                     */
   int32_t use_graph;          /* 1: one CUDA graph launch per batch          */
   int32_t chunk;              /* messages per device pass in hs_sign_batch   */
+  int32_t wots_from_tree;     /* 1: TREE_Sign records the signing leaf's
+                                 chains and WOTS_Sign gathers them; 0: WOTS_Sign
+                                 recomputes its chains (reference shape)     */
 } hs_set_config;
 
 HS_API int hs_open(int device, hs_t **out);

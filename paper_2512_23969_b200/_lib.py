@@ -43,6 +43,7 @@ class SetConfig(ctypes.Structure):
         ("variant", ctypes.c_int32 * 4),
         ("use_graph", ctypes.c_int32),
         ("chunk", ctypes.c_int32),
+        ("wots_from_tree", ctypes.c_int32),
     ]
 
 

@@ -49,6 +49,15 @@ cudaError_t launch(int set, int which, int variant, const LaunchArgs& a, cudaStr
   return cudaErrorInvalidValue;
 }
 
+size_t stash_words(int set) {
+  switch (set) {
+    case 0: return stash_words_per_msg<0>();
+    case 1: return stash_words_per_msg<1>();
+    case 2: return stash_words_per_msg<2>();
+  }
+  return 0;
+}
+
 size_t fors_smem(int set, int nt, int f, int relax) {
   switch (set) {
     case 0: return fors_smem_bytes<0>(nt, f, relax);
@@ -69,6 +78,7 @@ hs_set_config default_config(int set) {
   for (int i = 0; i < 4; i++) c.variant[i] = 0;
   c.use_graph = 1;
   c.chunk = 16384;
+  c.wots_from_tree = 1;
   return c;
 }
 
@@ -104,6 +114,7 @@ struct Buffers {
   uint16_t* idx = nullptr; size_t idx_cap = 0;
   uint32_t* roots = nullptr; size_t roots_cap = 0;
   uint32_t* froots = nullptr; size_t froots_cap = 0;
+  uint32_t* stash = nullptr; size_t stash_cap = 0;
   // pinned staging
   uint8_t* h_msgs = nullptr; size_t h_msgs_cap = 0;
   uint64_t* h_offs = nullptr; size_t h_offs_cap = 0;
@@ -167,8 +178,8 @@ bool valid_set(int set) { return set >= 0 && set <= 2; }
 
 std::string cfg_fingerprint(const hs_set_config& c) {
   char b[160];
-  snprintf(b, sizeof b, "%d/%d/%d/%d%d%d%d", c.fors_trees_per_set, c.fors_sets_fused, c.fors_relax, c.variant[0],
-           c.variant[1], c.variant[2], c.variant[3]);
+  snprintf(b, sizeof b, "%d/%d/%d/%d%d%d%d/%d", c.fors_trees_per_set, c.fors_sets_fused, c.fors_relax,
+           c.variant[0], c.variant[1], c.variant[2], c.variant[3], c.wots_from_tree);
   return b;
 }
 
@@ -191,13 +202,14 @@ int check_layout(hs_t* h, int set, const hs_set_config& c) {
   for (int i = 0; i < 4; i++)
     if (c.variant[i] != 0 && c.variant[i] != 1) return fail(h, HS_E_CONFIG, "variant must be 0 or 1");
   if (c.chunk < 1) return fail(h, HS_E_CONFIG, "chunk must be >= 1");
+  if (c.wots_from_tree != 0 && c.wots_from_tree != 1) return fail(h, HS_E_CONFIG, "wots_from_tree must be 0 or 1");
   return HS_OK;
 }
 
 int ensure_capacity(hs_t* h, int set, uint32_t count, size_t msg_bytes) {
   const SetInfo& I = kInfo[set];
   Buffers& B = h->buf[set];
-  void* before[9] = {B.msgs, B.offs, B.keyidx, B.optrand, B.sigs, B.plans, B.idx, B.roots, B.froots};
+  void* before[10] = {B.msgs, B.offs, B.keyidx, B.optrand, B.sigs, B.plans, B.idx, B.roots, B.froots, B.stash};
   CUDA_TRY(h, grow(B.msgs, B.msgs_cap, std::max(msg_bytes, (size_t)1)));
   CUDA_TRY(h, grow(B.offs, B.offs_cap, (size_t)count + 1));
   CUDA_TRY(h, grow(B.keyidx, B.keyidx_cap, (size_t)count));
@@ -207,7 +219,8 @@ int ensure_capacity(hs_t* h, int set, uint32_t count, size_t msg_bytes) {
   CUDA_TRY(h, grow(B.idx, B.idx_cap, (size_t)count * I.k));
   CUDA_TRY(h, grow(B.roots, B.roots_cap, (size_t)count * (I.d + 1) * 8));
   CUDA_TRY(h, grow(B.froots, B.froots_cap, (size_t)count * I.k * 8));
-  void* after[9] = {B.msgs, B.offs, B.keyidx, B.optrand, B.sigs, B.plans, B.idx, B.roots, B.froots};
+  if (h->sets[set].cfg.wots_from_tree) CUDA_TRY(h, grow(B.stash, B.stash_cap, (size_t)count * stash_words(set)));
+  void* after[10] = {B.msgs, B.offs, B.keyidx, B.optrand, B.sigs, B.plans, B.idx, B.roots, B.froots, B.stash};
   if (std::memcmp(before, after, sizeof before) != 0) {
     B.gen++;
     drop_graphs(h);
@@ -235,6 +248,7 @@ LaunchArgs make_args(hs_t* h, int set, uint32_t count) {
   a.fors_trees_per_set = St.cfg.fors_trees_per_set;
   a.fors_sets_fused = St.cfg.fors_sets_fused;
   a.fors_relax = St.cfg.fors_relax;
+  a.stash = (St.cfg.wots_from_tree && B.stash && B.stash_cap >= (size_t)count * stash_words(set)) ? B.stash : nullptr;
   return a;
 }
 
@@ -257,7 +271,7 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
     TRY(launch(set, K_TREE, c.variant[1], a, h->s0));
     TRY(rec(3, h->s0));
     TRY(rec(5, h->s0));
-    TRY(launch(set, K_WOTS, c.variant[2], a, h->s0));
+    TRY(launch(set, a.stash ? K_WOTS_GATHER : K_WOTS, c.variant[2], a, h->s0));
     TRY(rec(4, h->s0));
   } else {
     TRY(cudaEventRecord(h->fork, h->s0));
@@ -270,7 +284,7 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
     TRY(rec(3, h->s0));
     TRY(cudaStreamWaitEvent(h->s0, h->join, 0));
     TRY(rec(5, h->s0));
-    TRY(launch(set, K_WOTS, c.variant[2], a, h->s0));
+    TRY(launch(set, a.stash ? K_WOTS_GATHER : K_WOTS, c.variant[2], a, h->s0));
     TRY(rec(4, h->s0));
   }
 #undef TRY
@@ -392,7 +406,7 @@ void hs_close(hs_t* h) {
   for (int s = 0; s < 3; s++) {
     Buffers& B = h->buf[s];
     cudaFree(B.msgs); cudaFree(B.offs); cudaFree(B.keyidx); cudaFree(B.optrand); cudaFree(B.sigs);
-    cudaFree(B.plans); cudaFree(B.idx); cudaFree(B.roots); cudaFree(B.froots);
+    cudaFree(B.plans); cudaFree(B.idx); cudaFree(B.roots); cudaFree(B.froots); cudaFree(B.stash);
     cudaFreeHost(B.h_msgs); cudaFreeHost(B.h_offs); cudaFreeHost(B.h_sigs);
     cudaFree(h->sets[s].keys);
     cudaFree(h->sets[s].sk_raw);

@@ -18,6 +18,7 @@ enum KernelId : int {
   K_WOTS = 5,
   K_KEYGEN = 6,
   K_VERIFY = 7,
+  K_WOTS_GATHER = 8,
 };
 
 // variant: 0 = Native, 1 = Imad (sha256.cuh)
@@ -26,5 +27,8 @@ cudaError_t launch_kernel(int which, int variant, const LaunchArgs& a, cudaStrea
 
 template <int S>
 size_t fors_smem_bytes(int trees_per_set, int sets_fused, int relax);
+
+template <int S>
+size_t stash_words_per_msg();
 
 }  // namespace hs

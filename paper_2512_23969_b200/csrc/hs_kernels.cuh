@@ -59,6 +59,7 @@ struct LaunchArgs {
   uint32_t* roots;           // count * (d+1) * 8 words; slot 0 = FORS pk, slot l+1 = root of layer l
   uint32_t* fors_roots;      // count * k * 8 words
   uint8_t* sk_out;           // keygen output (nkeys * 4n)
+  uint32_t* stash;           // count * d * wots_len * w * NW words: signing-leaf chains (nullable)
   const uint8_t* pks;        // verify: nkeys * 2n (pk_seed || pk_root)
   const uint8_t* vsigs;      // verify: count * sig_bytes
   uint8_t* ok;               // verify: count flags
@@ -195,9 +196,11 @@ __device__ __forceinline__ void layer_coords(const MsgPlan& pl, int layer, uint6
 // One WOTS+ leaf (wots.py:119-143): wots_len chains of PRF + (w-1) F, then
 // T_len over the chain ends streamed through this thread's smem column.
 // ---------------------------------------------------------------------------
+// rec (nullable): wots_len x 16 nodes -- every chain position 0..15 of this
+// leaf, recorded when this leaf is the layer's signing leaf.
 template <int S, class V>
 __device__ __forceinline__ void wots_leaf(const KeyDev& K, uint32_t layer, uint64_t tree, uint32_t leaf,
-                                          uint32_t* column, int stride, uint32_t out[8]) {
+                                          uint32_t* column, int stride, uint32_t out[8], uint32_t* rec = nullptr) {
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
   uint32_t mid[8], sks[NW];
@@ -216,13 +219,12 @@ __device__ __forceinline__ void wots_leaf(const KeyDev& K, uint32_t layer, uint6
     uint32_t x[NW];
 #pragma unroll
     for (int j = 0; j < NW; j++) x[j] = st[j];
-#pragma unroll 1
-    for (int s = 0; s < Pr::w - 1; s++) {
-      adrs_set_chain_hash(wa, (uint32_t)i, (uint32_t)s);
-      thash_reg<V, NW>(st, mid, wa, x);
+    uint32_t* crec = rec ? rec + (size_t)i * Pr::w * NW : nullptr;
+    if (crec) {
 #pragma unroll
-      for (int j = 0; j < NW; j++) x[j] = st[j];
+      for (int j = 0; j < NW; j++) crec[j] = x[j];
     }
+    chain_F<V, NW>(x, mid, wa, 0u, (uint32_t)(Pr::w - 1), crec);
     ts.template push_node<NW>(x);
   }
   ts.finish(22u + (uint32_t)(Pr::wots_len * Pr::n));
@@ -240,7 +242,7 @@ template <int S, class V>
 __global__ void __launch_bounds__(kTreeBlock) tree_sign_kernel(LaunchArgs a) {
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
-  __shared__ uint32_t tbuf[16 * kTreeBlock];
+  __shared__ uint32_t tbuf[32 * kTreeBlock];
   const uint64_t per_msg = (uint64_t)Pr::d * Pr::leaves;
   const uint64_t gid = (uint64_t)blockIdx.x * kTreeBlock + threadIdx.x;
   const bool valid = gid < (uint64_t)a.count * per_msg;
@@ -257,7 +259,10 @@ __global__ void __launch_bounds__(kTreeBlock) tree_sign_kernel(LaunchArgs a) {
     const MsgPlan pl = a.plans[msg];
     K = &a.keys[pl.key];
     layer_coords<S>(pl, (int)layer, tree, leaf_idx);
-    wots_leaf<S, V>(*K, layer, tree, leaf, &tbuf[threadIdx.x], kTreeBlock, node);
+    uint32_t* rec = (a.stash && leaf == leaf_idx)
+                        ? a.stash + ((size_t)msg * Pr::d + layer) * Pr::wots_len * Pr::w * NW
+                        : nullptr;
+    wots_leaf<S, V>(*K, layer, tree, leaf, &tbuf[threadIdx.x], kTreeBlock, node, rec);
   }
   uint8_t* auth = a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_ht + (size_t)layer * Pr::layer_bytes +
                   Pr::wots_sig_bytes;
@@ -431,7 +436,7 @@ template <int S, class V>
 __global__ void __launch_bounds__(kSmallBlock) fors_pk_kernel(LaunchArgs a) {
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
-  __shared__ uint32_t tbuf[16 * kSmallBlock];
+  __shared__ uint32_t tbuf[32 * kSmallBlock];
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.count) return;
   const MsgPlan pl = a.plans[i];
@@ -504,13 +509,35 @@ __global__ void __launch_bounds__(kSmallBlock) wots_sign_kernel(LaunchArgs a) {
   uint32_t x[NW];
 #pragma unroll
   for (int j = 0; j < NW; j++) x[j] = st[j];
-#pragma unroll 1
-  for (uint32_t s = 0; s < digit; s++) {
-    adrs_set_chain_hash(wa, (uint32_t)chain, s);
-    thash_reg<V, NW>(st, mid, wa, x);
+  chain_F<V, NW>(x, mid, wa, 0u, digit);
+  store_node<NW>(a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_ht + (size_t)layer * Pr::layer_bytes + chain * Pr::n,
+                 x);
+}
+
+// WOTS+_Sign as a gather: TREE_Sign already walked every chain of each
+// layer's signing leaf (wots_gen_leaf computes the same values wots_sign
+// needs, wots.py:85-95 vs :119-143), so the signature chain i of layer l is
+// the recorded node at position digit_i.  Thread = (message, layer, chain).
+template <int S>
+__global__ void __launch_bounds__(kSmallBlock) wots_gather_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  constexpr int NW = Pr::NW;
+  const uint64_t per_msg = (uint64_t)Pr::d * Pr::wots_len;
+  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (uint64_t)a.count * per_msg) return;
+  const uint32_t msg = (uint32_t)(gid / per_msg);
+  const uint32_t rem = (uint32_t)(gid % per_msg);
+  const int layer = (int)(rem / Pr::wots_len);
+  const int chain = (int)(rem % Pr::wots_len);
+  uint32_t mw[8];
+  const uint32_t* r = a.roots + ((size_t)msg * (Pr::d + 1) + layer) * 8;
 #pragma unroll
-    for (int j = 0; j < NW; j++) x[j] = st[j];
-  }
+  for (int j = 0; j < NW; j++) mw[j] = r[j];
+  const uint32_t digit = wots_digit<S>(mw, chain);
+  const uint32_t* src = a.stash + ((((size_t)msg * Pr::d + layer) * Pr::wots_len + chain) * Pr::w + digit) * NW;
+  uint32_t x[NW];
+#pragma unroll
+  for (int j = 0; j < NW; j++) x[j] = src[j];
   store_node<NW>(a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_ht + (size_t)layer * Pr::layer_bytes + chain * Pr::n,
                  x);
 }
@@ -524,7 +551,7 @@ template <int S, class V>
 __global__ void __launch_bounds__(kTreeBlock) keygen_root_kernel(LaunchArgs a) {
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
-  __shared__ uint32_t tbuf[16 * kTreeBlock];
+  __shared__ uint32_t tbuf[32 * kTreeBlock];
   const uint64_t gid = (uint64_t)blockIdx.x * kTreeBlock + threadIdx.x;
   const bool valid = gid < (uint64_t)a.nkeys * Pr::leaves;
   const uint32_t key = valid ? (uint32_t)(gid / Pr::leaves) : 0u;
@@ -595,7 +622,7 @@ __global__ void __launch_bounds__(32 * kVerifyWarps) verify_kernel(LaunchArgs a)
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
   __shared__ uint32_t s_ends[kVerifyWarps][Pr::wots_len > Pr::k ? Pr::wots_len * NW : Pr::k * NW];
-  __shared__ uint32_t s_col[kVerifyWarps][16];
+  __shared__ uint32_t s_col[kVerifyWarps][32];
   __shared__ uint32_t s_root[kVerifyWarps][8];
   __shared__ uint32_t s_mid[kVerifyWarps][8];
   __shared__ uint64_t s_tree[kVerifyWarps];
@@ -696,10 +723,7 @@ __global__ void __launch_bounds__(32 * kVerifyWarps) verify_kernel(LaunchArgs a)
       uint32_t x[8];
       load_node<S>(wsig + c * Pr::n, x);
       Adrs wa = make_adrs((uint32_t)layer, tree, ADDR_WOTS, leaf_idx, (uint32_t)c, 0);
-      for (uint32_t s = digit; s < (uint32_t)(Pr::w - 1); s++) {
-        adrs_set_chain_hash(wa, (uint32_t)c, s);
-        thash_reg<V, NW>(x, mid, wa, x);
-      }
+      chain_F<V, NW>(x, mid, wa, digit, (uint32_t)(Pr::w - 1) - digit);
       for (int j = 0; j < NW; j++) s_ends[warp][c * NW + j] = x[j];
     }
     __syncwarp();

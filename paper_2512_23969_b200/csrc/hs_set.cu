@@ -51,6 +51,9 @@ cudaError_t launch_v(int which, const LaunchArgs& a, cudaStream_t s) {
     case K_KEYGEN:
       keygen_root_kernel<S, V><<<blocks((uint64_t)a.nkeys * Pr::leaves, kTreeBlock), kTreeBlock, 0, s>>>(a);
       break;
+    case K_WOTS_GATHER:
+      wots_gather_kernel<S><<<blocks((uint64_t)a.count * Pr::d * Pr::wots_len, kSmallBlock), kSmallBlock, 0, s>>>(a);
+      break;
     case K_VERIFY:
       verify_kernel<S, V><<<blocks(a.count, kVerifyWarps), 32 * kVerifyWarps, 0, s>>>(a);
       break;
@@ -65,6 +68,11 @@ cudaError_t launch_v(int which, const LaunchArgs& a, cudaStream_t s) {
 template <>
 cudaError_t launch_kernel<HS_SET>(int which, int variant, const LaunchArgs& a, cudaStream_t s) {
   return variant ? launch_v<HS_SET, Imad>(which, a, s) : launch_v<HS_SET, Native>(which, a, s);
+}
+
+template <>
+size_t stash_words_per_msg<HS_SET>() {
+  return (size_t)P<HS_SET>::d * P<HS_SET>::wots_len * P<HS_SET>::w * P<HS_SET>::NW;
 }
 
 template <>

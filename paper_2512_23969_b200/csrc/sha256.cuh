@@ -46,44 +46,149 @@ __device__ __forceinline__ constexpr uint32_t IVc(int i) {
 
 // ---------------------------------------------------------------------------
 // arithmetic paths
+//
+// SHA-256 on sm_100a is bound by the ALU pipe (SHF/LOP3/IADD3/PRMT; 16
+// lanes/clk/SMSP) while the FMA pipe (IMAD family, also 16 lanes/clk/SMSP)
+// idles.  A path decides, per operation site, which pipe does the work:
+//   fma_add(a,b)   a*one+b            IMAD      (one from the constant bank)
+//   fma_shr(x,r)   hi(x * 2^(32-r))   IMAD.HI
+//   fma_rotr(x,r)  hi(x*m) + lo(x*m), m = 2^(32-r)   IMAD + IMAD.HI
+// Multipliers live in constant memory so ptxas cannot fold them back into
+// shifts.  Native leaves every choice to ptxas; Imad moves all adds; Mix<>
+// moves a chosen subset of rotates / shifts / two-input adds.
 // ---------------------------------------------------------------------------
-struct Native {
-  static constexpr int id = 0;
-  static __device__ __forceinline__ uint32_t add(uint32_t a, uint32_t b) { return a + b; }
-};
-
-struct Imad {
-  static constexpr int id = 1;
-  static __device__ __forceinline__ uint32_t add(uint32_t a, uint32_t b) { return a * c_one + b; }
-};
+static __constant__ uint32_t c_pow2[33] = {
+    1u << 0,  1u << 1,  1u << 2,  1u << 3,  1u << 4,  1u << 5,  1u << 6,  1u << 7,  1u << 8,
+    1u << 9,  1u << 10, 1u << 11, 1u << 12, 1u << 13, 1u << 14, 1u << 15, 1u << 16, 1u << 17,
+    1u << 18, 1u << 19, 1u << 20, 1u << 21, 1u << 22, 1u << 23, 1u << 24, 1u << 25, 1u << 26,
+    1u << 27, 1u << 28, 1u << 29, 1u << 30, 1u << 31, 0u};
 
 __device__ __forceinline__ uint32_t rotr(uint32_t x, int r) { return __funnelshift_r(x, x, r); }
-__device__ __forceinline__ uint32_t bsig0(uint32_t a) { return rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22); }
-__device__ __forceinline__ uint32_t bsig1(uint32_t e) { return rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25); }
-__device__ __forceinline__ uint32_t ssig0(uint32_t x) { return rotr(x, 7) ^ rotr(x, 18) ^ (x >> 3); }
-__device__ __forceinline__ uint32_t ssig1(uint32_t x) { return rotr(x, 17) ^ rotr(x, 19) ^ (x >> 10); }
+__device__ __forceinline__ uint32_t fma_add(uint32_t a, uint32_t b) { return a * c_one + b; }
+__device__ __forceinline__ uint32_t fma_shr(uint32_t x, int r) { return __umulhi(x, c_pow2[32 - r]); }
+__device__ __forceinline__ uint32_t fma_rotr(uint32_t x, int r) {
+  const uint32_t m = c_pow2[32 - r];
+  const uint32_t lo = x * m;
+  uint32_t out;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(out) : "r"(x), "r"(m), "r"(lo));
+  return out;
+}
 __device__ __forceinline__ uint32_t ch(uint32_t e, uint32_t f, uint32_t g) { return g ^ (e & (f ^ g)); }
 __device__ __forceinline__ uint32_t maj(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
 
+// rotation helper: the first NF rotations of a sigma run on the FMA pipe
+template <int NF, int IDX>
+__device__ __forceinline__ uint32_t rot_sel(uint32_t x, int r) { return IDX < NF ? fma_rotr(x, r) : rotr(x, r); }
+
+struct Native {
+  static constexpr int id = 0;
+  static __device__ __forceinline__ uint32_t S0(uint32_t a) { return rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22); }
+  static __device__ __forceinline__ uint32_t S1(uint32_t e) { return rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25); }
+  static __device__ __forceinline__ uint32_t s0(uint32_t x) { return rotr(x, 7) ^ rotr(x, 18) ^ (x >> 3); }
+  static __device__ __forceinline__ uint32_t s1(uint32_t x) { return rotr(x, 17) ^ rotr(x, 19) ^ (x >> 10); }
+  static __device__ __forceinline__ uint32_t t1(uint32_t h, uint32_t k, uint32_t w, uint32_t s1v, uint32_t chv) {
+    return h + k + w + s1v + chv;
+  }
+  static __device__ __forceinline__ uint32_t enew(uint32_t d, uint32_t t) { return d + t; }
+  static __device__ __forceinline__ uint32_t anew(uint32_t t, uint32_t s0v, uint32_t mj) { return t + s0v + mj; }
+  static __device__ __forceinline__ uint32_t wnew(uint32_t s1v, uint32_t w7, uint32_t s0v, uint32_t w16) {
+    return s1v + w7 + s0v + w16;
+  }
+  static __device__ __forceinline__ uint32_t ff(uint32_t x, uint32_t y) { return x + y; }
+};
+
+struct Imad : Native {
+  static constexpr int id = 1;
+  static __device__ __forceinline__ uint32_t t1(uint32_t h, uint32_t k, uint32_t w, uint32_t s1v, uint32_t chv) {
+    return fma_add(fma_add(fma_add(h, k), w), fma_add(s1v, chv));
+  }
+  static __device__ __forceinline__ uint32_t enew(uint32_t d, uint32_t t) { return fma_add(d, t); }
+  static __device__ __forceinline__ uint32_t anew(uint32_t t, uint32_t s0v, uint32_t mj) {
+    return fma_add(t, fma_add(s0v, mj));
+  }
+  static __device__ __forceinline__ uint32_t wnew(uint32_t s1v, uint32_t w7, uint32_t s0v, uint32_t w16) {
+    return fma_add(fma_add(s1v, w7), fma_add(s0v, w16));
+  }
+  static __device__ __forceinline__ uint32_t ff(uint32_t x, uint32_t y) { return fma_add(x, y); }
+};
+
+// Mix<NS1, NS0, NSS, SHR, EADD>: NS1/NS0 rotations of Sigma1/Sigma0 and NSS of
+// each schedule sigma on the FMA pipe; SHR: the schedule's plain shifts via
+// IMAD.HI; EADD: the two-input adds (e = d + T1, the 4th schedule term, the
+// feed-forward) via IMAD; three-input adds stay IADD3.
+template <int NS1, int NS0, int NSS, bool SHR, bool EADD>
+struct Mix : Native {
+  static constexpr int id = 2;
+  static __device__ __forceinline__ uint32_t S0(uint32_t a) {
+    return rot_sel<NS0, 0>(a, 2) ^ rot_sel<NS0, 1>(a, 13) ^ rot_sel<NS0, 2>(a, 22);
+  }
+  static __device__ __forceinline__ uint32_t S1(uint32_t e) {
+    return rot_sel<NS1, 0>(e, 6) ^ rot_sel<NS1, 1>(e, 11) ^ rot_sel<NS1, 2>(e, 25);
+  }
+  static __device__ __forceinline__ uint32_t s0(uint32_t x) {
+    return rot_sel<NSS, 0>(x, 7) ^ rot_sel<NSS, 1>(x, 18) ^ (SHR ? fma_shr(x, 3) : (x >> 3));
+  }
+  static __device__ __forceinline__ uint32_t s1(uint32_t x) {
+    return rot_sel<NSS, 0>(x, 17) ^ rot_sel<NSS, 1>(x, 19) ^ (SHR ? fma_shr(x, 10) : (x >> 10));
+  }
+  static __device__ __forceinline__ uint32_t enew(uint32_t d, uint32_t t) { return EADD ? fma_add(d, t) : d + t; }
+  static __device__ __forceinline__ uint32_t wnew(uint32_t s1v, uint32_t w7, uint32_t s0v, uint32_t w16) {
+    return EADD ? fma_add(s1v + w7 + s0v, w16) : s1v + w7 + s0v + w16;
+  }
+  static __device__ __forceinline__ uint32_t ff(uint32_t x, uint32_t y) { return EADD ? fma_add(x, y) : x + y; }
+};
+
+// Rounds [R0, R1) of SHA-256 on working state s, expanding the schedule in
+// place for rounds >= 16.  Fully unrolled so constant message words
+// (padding, lengths, zeros, chain-invariant ADRS words) fold.
+template <class V, int R0, int R1>
+__device__ __forceinline__ void sha_rounds(uint32_t s[8], uint32_t* W) {
+  uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5], g = s[6], h = s[7];
+#pragma unroll
+  for (int i = R0; i < R1; i++) {
+    if (i >= 16) {
+      W[i & 15] = V::wnew(V::s1(W[(i - 2) & 15]), W[(i - 7) & 15], V::s0(W[(i - 15) & 15]), W[i & 15]);
+    }
+    const uint32_t t = V::t1(h, Kc(i), W[i & 15], V::S1(e), ch(e, f, g));
+    const uint32_t an = V::anew(t, V::S0(a), maj(a, b, c));
+    h = g; g = f; f = e; e = V::enew(d, t);
+    d = c; c = b; b = a; a = an;
+  }
+  s[0] = a; s[1] = b; s[2] = c; s[3] = d; s[4] = e; s[5] = f; s[6] = g; s[7] = h;
+}
+
 // One SHA-256 compression; W is consumed (used as the rolling schedule).
-// Fully unrolled so that constant message words (padding, lengths, zeros)
-// fold into the schedule.
 template <class V>
 __device__ __forceinline__ void compress(uint32_t st[8], uint32_t W[16]) {
-  uint32_t a = st[0], b = st[1], c = st[2], d = st[3], e = st[4], f = st[5], g = st[6], h = st[7];
+  uint32_t s[8];
 #pragma unroll
-  for (int i = 0; i < 64; i++) {
-    if (i >= 16) {
-      W[i & 15] = V::add(V::add(ssig1(W[(i - 2) & 15]), W[(i - 7) & 15]),
-                         V::add(ssig0(W[(i - 15) & 15]), W[i & 15]));
-    }
-    uint32_t t1 = V::add(V::add(V::add(h, Kc(i)), W[i & 15]), V::add(bsig1(e), ch(e, f, g)));
-    uint32_t t2 = V::add(bsig0(a), maj(a, b, c));
-    h = g; g = f; f = e; e = V::add(d, t1);
-    d = c; c = b; b = a; a = V::add(t1, t2);
-  }
-  st[0] = V::add(st[0], a); st[1] = V::add(st[1], b); st[2] = V::add(st[2], c); st[3] = V::add(st[3], d);
-  st[4] = V::add(st[4], e); st[5] = V::add(st[5], f); st[6] = V::add(st[6], g); st[7] = V::add(st[7], h);
+  for (int i = 0; i < 8; i++) s[i] = st[i];
+  sha_rounds<V, 0, 64>(s, W);
+#pragma unroll
+  for (int i = 0; i < 8; i++) st[i] = V::ff(st[i], s[i]);
+}
+
+// Rounds [0, R) only (no schedule expansion needed while R <= 16).
+template <class V, int R>
+__device__ __forceinline__ void rounds_prefix(uint32_t s[8], const uint32_t* W) {
+  static_assert(R <= 16, "prefix rounds read W directly");
+  uint32_t Wc[16];
+#pragma unroll
+  for (int i = 0; i < R; i++) Wc[i] = W[i];
+  sha_rounds<V, 0, R>(s, Wc);
+}
+
+// Compression resumed after R0 rounds: `sR` is the working state after rounds
+// [0, R0) (computed once by rounds_prefix while W[0..R0) stay fixed), `st`
+// the chaining value for the feed-forward.  W must still hold all 16 words.
+template <class V, int R0>
+__device__ __forceinline__ void compress_resume(uint32_t st[8], const uint32_t sR[8], uint32_t W[16]) {
+  uint32_t s[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) s[i] = sR[i];
+  sha_rounds<V, R0, 64>(s, W);
+#pragma unroll
+  for (int i = 0; i < 8; i++) st[i] = V::ff(st[i], s[i]);
 }
 
 // ---------------------------------------------------------------------------
@@ -143,6 +248,47 @@ __device__ __forceinline__ void thash_reg(uint32_t st[8], const uint32_t mid[8],
   }
 }
 
+// WOTS+ chain (wots.py:42-60): `steps` applications of F starting at hash
+// index `start`, x updated in place.  Along a chain only ADRS bytes 20..21
+// (the hash index, < 2^16) and the node change, so message words W0..W4 are
+// fixed and SHA-256 rounds 0-4 are computed once per chain, not per step.
+// When `rec` is non-null, the node after step s is also stored at
+// rec[(s + 1) * NW ...] (TREE_Sign keeps the signing leaf's chain so that
+// WOTS_Sign becomes a gather).
+template <class V, int NW>
+__device__ __forceinline__ void chain_F(uint32_t* x, const uint32_t mid[8], const Adrs& a, uint32_t start,
+                                        uint32_t steps, uint32_t* rec = nullptr) {
+  constexpr int total = 22 + 4 * NW;
+  static_assert(total + 9 <= 64, "F is a single block after the midstate");
+  uint32_t pre[8];
+  const uint32_t W04[5] = {a.w0, a.w1, a.w2, a.w3, a.w4};
+#pragma unroll
+  for (int i = 0; i < 8; i++) pre[i] = mid[i];
+  rounds_prefix<V, 5>(pre, W04);
+#pragma unroll 1
+  for (uint32_t s = start; s < start + steps; s++) {
+    uint32_t W[16];
+    W[0] = a.w0; W[1] = a.w1; W[2] = a.w2; W[3] = a.w3; W[4] = a.w4;
+    W[5] = join16(s, x[0]);
+#pragma unroll
+    for (int j = 1; j < NW; j++) W[5 + j] = join16(x[j - 1], x[j]);
+    W[5 + NW] = (x[NW - 1] << 16) | 0x8000u;
+#pragma unroll
+    for (int j = 6 + NW; j < 15; j++) W[j] = 0;
+    W[15] = (uint32_t)((64 + total) * 8);
+    uint32_t st[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) st[i] = mid[i];
+    compress_resume<V, 5>(st, pre, W);
+#pragma unroll
+    for (int j = 0; j < NW; j++) x[j] = st[j];
+    if (rec) {
+#pragma unroll
+      for (int j = 0; j < NW; j++) rec[(s + 1) * NW + j] = x[j];
+    }
+  }
+}
+
 // PRF(SK.seed, ADRS) = SHA-256(SK.seed || ADRS)[:n] from the IV (hashes.py:139-150).
 template <class V, int NW>
 __device__ __forceinline__ void prf_reg(uint32_t st[8], const uint32_t* sk_seed, const Adrs& a) {
@@ -160,16 +306,19 @@ __device__ __forceinline__ void prf_reg(uint32_t st[8], const uint32_t* sk_seed,
 }
 
 // ---------------------------------------------------------------------------
-// Streaming tweakable hash over many nodes (T_len, T_k).  The 16-word block
-// under construction lives in a caller-provided column (shared memory, one
-// word every `stride` words so a warp's columns are bank-conflict free).
-// The write position is warp-uniform in every caller.
+// Streaming tweakable hash over many nodes (T_len, T_k).  Message words go
+// into a 32-word ring (two SHA blocks) in a caller-provided column of shared
+// memory (one word every `stride` words, so a warp's columns are bank-
+// conflict free); a block is compressed as soon as it is complete.  Write
+// positions are warp-uniform in every caller, and there are exactly two
+// compression sites (push_node, finish) to keep the kernels' code small.
 // ---------------------------------------------------------------------------
 template <class V>
 struct TStream {
   uint32_t st[8];
   uint32_t carry;
-  int pos;
+  uint32_t pos;   // absolute word index of the next write
+  uint32_t done;  // absolute word index of the next block not yet compressed
   uint32_t* buf;
   int stride;
 
@@ -181,32 +330,35 @@ struct TStream {
     buf[0] = a.w0; buf[stride] = a.w1; buf[2 * stride] = a.w2; buf[3 * stride] = a.w3; buf[4 * stride] = a.w4;
     carry = a.h5;
     pos = 5;
+    done = 0;
   }
-  __device__ __forceinline__ void flush() {
+  __device__ __forceinline__ void put(uint32_t at, uint32_t w) { buf[(at & 31u) * stride] = w; }
+  __device__ __forceinline__ void compress_block() {
     uint32_t W[16];
+    const uint32_t base = done & 31u;
 #pragma unroll
-    for (int j = 0; j < 16; j++) W[j] = buf[j * stride];
+    for (int j = 0; j < 16; j++) W[j] = buf[(base + j) * stride];
     compress<V>(st, W);
-    pos = 0;
-  }
-  __device__ __forceinline__ void push(uint32_t w) {
-    buf[pos * stride] = w;
-    if (++pos == 16) flush();
+    done += 16;
   }
   template <int NW>
   __device__ __forceinline__ void push_node(const uint32_t* x) {
 #pragma unroll
     for (int j = 0; j < NW; j++) {
-      push((carry << 16) | (x[j] >> 16));
+      put(pos + j, (carry << 16) | (x[j] >> 16));
       carry = x[j] & 0xFFFFu;
     }
+    pos += NW;
+    if (pos >= done + 16) compress_block();
   }
   // total_bytes: bytes after the midstate block (22 + message length)
   __device__ __forceinline__ void finish(uint32_t total_bytes) {
-    push((carry << 16) | 0x8000u);
-    while (pos != 14) push(0u);
-    push(0u);
-    push((64u + total_bytes) * 8u);
+    put(pos++, (carry << 16) | 0x8000u);
+    const uint32_t end = ((pos & 15u) <= 14u ? (pos | 15u) + 1u : (pos | 15u) + 17u);
+    while (pos < end - 1) put(pos++, 0u);
+    put(pos++, (64u + total_bytes) * 8u);
+#pragma unroll 1
+    while (done < end) compress_block();
   }
 };
 

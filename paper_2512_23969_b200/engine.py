@@ -88,6 +88,7 @@ class Engine:
             "variant": {k: int(c.variant[i]) for i, k in enumerate(KERNELS)},
             "use_graph": bool(c.use_graph),
             "chunk": c.chunk,
+            "wots_from_tree": bool(c.wots_from_tree),
         }
 
     def set_config(self, set_id: str, **kw) -> dict:
@@ -103,6 +104,7 @@ class Engine:
             c.variant[i] = int(variant[k])
         c.use_graph = int(bool(cur["use_graph"]))
         c.chunk = int(cur["chunk"])
+        c.wots_from_tree = int(bool(cur["wots_from_tree"]))
         self._check(_lib.lib().hs_config_set(self._h, SET_INDEX[set_id], ctypes.byref(c)), "hs_config_set")
         return self.config(set_id)
 

@@ -79,7 +79,8 @@ def test_mixed_batch_vs_oracle(eng, oracle_mod, set_id):
 
 @pytest.mark.parametrize("set_id", SETS)
 @pytest.mark.parametrize("variant", [0, 1])
-def test_layouts_and_variants(eng, oracle_mod, set_id, variant):
+@pytest.mark.parametrize("stash", [True, False])
+def test_layouts_and_variants(eng, oracle_mod, set_id, variant, stash):
     """Every FORS fusion layout / relax mode and both SHA-256 paths give identical bytes."""
     p = derive(set_id)
     rng = random.Random(99)
@@ -93,7 +94,7 @@ def test_layouts_and_variants(eng, oracle_mod, set_id, variant):
                "256f": [(1, 1, 0), (2, 2, 1), (1, 5, 1), (4, 1, 1)]}[set_id]
     try:
         for nt, f, rx in layouts:
-            eng.set_config(set_id, fors_trees_per_set=nt, fors_sets_fused=f, fors_relax=bool(rx),
+            eng.set_config(set_id, fors_trees_per_set=nt, fors_sets_fused=f, fors_relax=bool(rx), wots_from_tree=stash,
                            variant={k: variant for k in ("FORS_Sign", "TREE_Sign", "WOTS_Sign", "host")})
             assert eng.sign_batch(set_id, msgs) == ref, (nt, f, rx)
     finally:

@@ -1,0 +1,115 @@
+// sha_probe.cu -- throughput of the WOTS chain step (F) under each SHA-256
+// arithmetic path of csrc/sha256.cuh, plus 2-way chain interleaving.
+// Reports compressions/s and checks every path against Native bit-for-bit.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../paper_2512_23969_b200/csrc/sha256.cuh"
+
+using namespace hs;
+
+template <class V, int ILP, int NT>
+__global__ void __launch_bounds__(NT) chain_kernel(uint32_t* out, int reps) {
+  constexpr int NW = 4;
+  uint32_t mid[8];
+  for (int i = 0; i < 8; i++) mid[i] = 0x6a09e667u * (i + 1);
+  uint32_t x[ILP][NW];
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int c = 0; c < ILP; c++)
+    for (int j = 0; j < NW; j++) x[c][j] = tid * 2654435761u + 17u * j + 1000003u * c;
+  for (int r = 0; r < reps; r++) {
+    Adrs a[ILP];
+    for (int c = 0; c < ILP; c++) a[c] = make_adrs(3, tid + r, 0u, c, r & 63, 0);
+    if (ILP == 1) {
+      chain_F<V, NW>(x[0], mid, a[0], 0u, 15u);
+    } else {
+      uint32_t pre[ILP][8];
+      for (int c = 0; c < ILP; c++) {
+        const uint32_t W04[5] = {a[c].w0, a[c].w1, a[c].w2, a[c].w3, a[c].w4};
+        for (int i = 0; i < 8; i++) pre[c][i] = mid[i];
+        rounds_prefix<V, 5>(pre[c], W04);
+      }
+#pragma unroll 1
+      for (uint32_t s = 0; s < 15; s++) {
+#pragma unroll
+        for (int c = 0; c < ILP; c++) {
+          uint32_t W[16];
+          W[0] = a[c].w0; W[1] = a[c].w1; W[2] = a[c].w2; W[3] = a[c].w3; W[4] = a[c].w4;
+          W[5] = join16(s, x[c][0]);
+          for (int j = 1; j < NW; j++) W[5 + j] = join16(x[c][j - 1], x[c][j]);
+          W[5 + NW] = (x[c][NW - 1] << 16) | 0x8000u;
+          for (int j = 6 + NW; j < 15; j++) W[j] = 0;
+          W[15] = (64 + 22 + 4 * NW) * 8;
+          uint32_t st[8];
+          for (int i = 0; i < 8; i++) st[i] = mid[i];
+          compress_resume<V, 5>(st, pre[c], W);
+          for (int j = 0; j < NW; j++) x[c][j] = st[j];
+        }
+      }
+    }
+  }
+  for (int c = 0; c < ILP; c++)
+    for (int j = 0; j < NW; j++) out[((size_t)tid * ILP + c) * NW + j] = x[c][j];
+}
+
+static uint32_t* g_ref = nullptr;
+
+template <class V, int ILP, int NT = 128>
+void run(const char* name) {
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int blocks = sms * 64 / ILP, reps = 8;
+  const size_t threads = (size_t)blocks * NT;
+  uint32_t* out;
+  cudaMalloc(&out, threads * ILP * 4 * 4);
+  chain_kernel<V, ILP, NT><<<blocks, NT>>>(out, 1);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  chain_kernel<V, ILP, NT><<<blocks, NT>>>(out, reps);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaError_t e = cudaGetLastError();
+  double comps = (double)threads * ILP * reps * 15;
+  // correctness vs Native ILP=1 on the first chain of each thread
+  uint32_t* h = (uint32_t*)malloc(threads * ILP * 16);
+  cudaMemcpy(h, out, threads * ILP * 16, cudaMemcpyDeviceToHost);
+  int bad = 0;
+  if (!g_ref) {
+    g_ref = h;
+  } else if (ILP == 1) {
+    for (size_t i = 0; i < threads * 4; i++) bad += h[i] != g_ref[i];
+    free(h);
+  } else {
+    free(h);
+  }
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, chain_kernel<V, ILP, NT>);
+  printf("%-34s ILP=%d regs=%3d  %8.3f Gcomp/s  (%.2f ms)  %s%s\n", name, ILP, fa.numRegs, comps / ms / 1e6, ms,
+         bad ? "MISMATCH " : "", e != cudaSuccess ? cudaGetErrorString(e) : "");
+  cudaFree(out);
+}
+
+int main() {
+  run<Native, 1>("Native");
+  run<Imad, 1>("Imad");
+  run<Mix<0, 0, 0, true, false>, 1>("Mix<0,0,0,shr,->");
+  run<Mix<0, 0, 0, true, true>, 1>("Mix<0,0,0,shr,eadd>");
+  run<Mix<1, 0, 0, true, true>, 1>("Mix<1,0,0,shr,eadd>");
+  run<Mix<1, 1, 0, true, true>, 1>("Mix<1,1,0,shr,eadd>");
+  run<Mix<1, 1, 1, true, true>, 1>("Mix<1,1,1,shr,eadd>");
+  run<Mix<2, 1, 1, true, true>, 1>("Mix<2,1,1,shr,eadd>");
+  run<Mix<2, 2, 1, true, true>, 1>("Mix<2,2,1,shr,eadd>");
+  run<Mix<1, 1, 0, true, false>, 1>("Mix<1,1,0,shr,->");
+  run<Mix<1, 0, 1, true, true>, 1>("Mix<1,0,1,shr,eadd>");
+  run<Native, 2>("Native");
+  run<Mix<1, 1, 0, true, true>, 2>("Mix<1,1,0,shr,eadd>");
+  run<Mix<1, 1, 1, true, true>, 2>("Mix<1,1,1,shr,eadd>");
+  run<Mix<2, 1, 1, true, true>, 2>("Mix<2,1,1,shr,eadd>");
+  run<Native, 1, 256>("Native NT256");
+  run<Mix<1, 1, 0, true, true>, 1, 256>("Mix<1,1,0,shr,eadd> NT256");
+  return 0;
+}
