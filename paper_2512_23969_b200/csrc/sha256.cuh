@@ -2,15 +2,16 @@
 //
 // Replaces the reference's two bit-identical compression backends
 // (backends.py:51-123, selected per (kernel,set) by BackendSelection
-// backends.py:201-257) with two compile-time arithmetic paths:
+// backends.py:201-257) with compile-time arithmetic paths:
 //
 //   Native : plain C; ptxas picks IADD3/LOP3/SHF (ALU pipe) for almost all.
-//   Imad   : every 32-bit add is written as a*one+b with `one` read from the
-//            constant bank, so ptxas must emit IMAD (FMA pipe).  SHA-256 is
-//            ALU-pipe bound on Blackwell (SHF+LOP3 have nowhere else to go);
-//            moving the ~360 adds per compression to the otherwise idle FMA
-//            pipe is the sm_100a analog of the paper's `mad.lo.u32` PTX path
-//            (PAPER.md:341-382).
+//   Fast   : Mix<0,0,0,SHR,1,ANF,-> -- the schedule shifts as IMAD.HI (inline
+//            PTX mad.hi) and the 3-input adds of T1 and `a` as IMAD chains with
+//            an opaque constant-bank multiplier, moving work from the
+//            saturated ALU pipe to the idle FMA pipe (the sm_100a analog of
+//            the paper's `mad.lo.u32` PTX path).  Chosen by
+//            tools/sha_probe.cu on B200: 17.2 vs 15.5 G chain-steps/s.
+//   Imad / other Mix<...>: kept for the probe.
 //
 // Tweakable hashes follow hashes.py:124-150: thash = SHA-256(PKseed-midstate,
 // ADRS(22B) || M)[:n]; PRF = SHA-256(SKseed || ADRS)[:n] from the IV.  Nodes
@@ -73,6 +74,9 @@ __device__ __forceinline__ uint32_t fma_rotr(uint32_t x, int r) {
   asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(out) : "r"(x), "r"(m), "r"(lo));
   return out;
 }
+// x + K for a compile-time K: one * K + x with `one` opaque, so ptxas keeps
+// it on the FMA pipe as IMAD Rd, Rone, K, Rx.
+__device__ __forceinline__ uint32_t fma_addk(uint32_t x, uint32_t k) { return c_one * k + x; }
 __device__ __forceinline__ uint32_t ch(uint32_t e, uint32_t f, uint32_t g) { return g ^ (e & (f ^ g)); }
 __device__ __forceinline__ uint32_t maj(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
 
@@ -112,11 +116,14 @@ struct Imad : Native {
   static __device__ __forceinline__ uint32_t ff(uint32_t x, uint32_t y) { return fma_add(x, y); }
 };
 
-// Mix<NS1, NS0, NSS, SHR, EADD>: NS1/NS0 rotations of Sigma1/Sigma0 and NSS of
-// each schedule sigma on the FMA pipe; SHR: the schedule's plain shifts via
-// IMAD.HI; EADD: the two-input adds (e = d + T1, the 4th schedule term, the
-// feed-forward) via IMAD; three-input adds stay IADD3.
-template <int NS1, int NS0, int NSS, bool SHR, bool EADD>
+// Mix<NS1, NS0, NSS, SHR, T1F, ANF, WF>: NS1/NS0 rotations of Sigma1/Sigma0
+// and NSS of each schedule sigma on the FMA pipe (IMAD + IMAD.HI); SHR: the
+// schedule's plain shifts via IMAD.HI; T1F (0..2) of the two 3-input adds of
+// T1, ANF the 3-input add of the new `a`, WF the schedule sum split into
+// IMADs.  Two-input adds (e = d + T1, feed-forward) always use IMAD.
+// Measured on B200 (tools/sha_probe.cu): IMAD issues at the ALU rate on the
+// FMA pipe, IMAD.HI at half rate; ALU and FMA pipes dual-issue.
+template <int NS1, int NS0, int NSS, bool SHR, int T1F, bool ANF, bool WF>
 struct Mix : Native {
   static constexpr int id = 2;
   static __device__ __forceinline__ uint32_t S0(uint32_t a) {
@@ -131,12 +138,23 @@ struct Mix : Native {
   static __device__ __forceinline__ uint32_t s1(uint32_t x) {
     return rot_sel<NSS, 0>(x, 17) ^ rot_sel<NSS, 1>(x, 19) ^ (SHR ? fma_shr(x, 10) : (x >> 10));
   }
-  static __device__ __forceinline__ uint32_t enew(uint32_t d, uint32_t t) { return EADD ? fma_add(d, t) : d + t; }
-  static __device__ __forceinline__ uint32_t wnew(uint32_t s1v, uint32_t w7, uint32_t s0v, uint32_t w16) {
-    return EADD ? fma_add(s1v + w7 + s0v, w16) : s1v + w7 + s0v + w16;
+  static __device__ __forceinline__ uint32_t t1(uint32_t h, uint32_t k, uint32_t w, uint32_t s1v, uint32_t chv) {
+    if (T1F == 0) return h + k + w + s1v + chv;
+    if (T1F == 1) return fma_add(h + k + w, fma_add(s1v, chv));
+    if (T1F == 2) return fma_add(fma_add(fma_add(w, h), k), fma_add(s1v, chv));
+    return fma_add(fma_add(w, fma_addk(h, k)), fma_add(s1v, chv));
   }
-  static __device__ __forceinline__ uint32_t ff(uint32_t x, uint32_t y) { return EADD ? fma_add(x, y) : x + y; }
+  static __device__ __forceinline__ uint32_t enew(uint32_t d, uint32_t t) { return fma_add(d, t); }
+  static __device__ __forceinline__ uint32_t anew(uint32_t t, uint32_t s0v, uint32_t mj) {
+    return ANF ? fma_add(t, fma_add(s0v, mj)) : t + s0v + mj;
+  }
+  static __device__ __forceinline__ uint32_t wnew(uint32_t s1v, uint32_t w7, uint32_t s0v, uint32_t w16) {
+    return WF ? fma_add(fma_add(s1v, w7), fma_add(s0v, w16)) : fma_add(s1v + w7 + s0v, w16);
+  }
+  static __device__ __forceinline__ uint32_t ff(uint32_t x, uint32_t y) { return fma_add(x, y); }
 };
+
+using Fast = Mix<0, 0, 0, true, 1, true, false>;
 
 // Rounds [R0, R1) of SHA-256 on working state s, expanding the schedule in
 // place for rounds >= 16.  Fully unrolled so constant message words

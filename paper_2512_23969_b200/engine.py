@@ -266,11 +266,31 @@ _ENGINES: dict[int, Engine] = {}
 _ENGINES_LOCK = threading.Lock()
 
 
+TUNED_CONFIG = _lib.PKG_DIR / "b200_tuned.json"
+
+
+def apply_tuned_config(eng: Engine, path=None) -> bool:
+    """Apply $HERO_SIGN_CONFIG, else the packaged on-device tuning result
+    (b200_tuned.json written by tools/tune_all.py on a B200), if present."""
+    import os
+
+    from .config import ENV_CONFIG_PATH, TuningConfig
+
+    path = path or os.environ.get(ENV_CONFIG_PATH) or (TUNED_CONFIG if TUNED_CONFIG.exists() else None)
+    if not path:
+        return False
+    TuningConfig.load(path).apply(eng)
+    return True
+
+
 def get_engine(device: int | None = None) -> Engine:
-    """Process-wide engine for a device (default: $HEROSIGN_DEVICE / $LOCAL_RANK / 0)."""
+    """Process-wide engine for a device (default: $HEROSIGN_DEVICE / $LOCAL_RANK / 0),
+    configured from the persisted tuning result when one exists."""
     dev = _lib.default_device() if device is None else int(device)
     with _ENGINES_LOCK:
         eng = _ENGINES.get(dev)
         if eng is None:
-            eng = _ENGINES[dev] = Engine(dev)
+            eng = Engine(dev)
+            apply_tuned_config(eng)
+            _ENGINES[dev] = eng
         return eng

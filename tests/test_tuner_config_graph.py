@@ -1,0 +1,157 @@
+"""CPU checks for the tuner (Algorithm 1), the config JSON and the task-graph scheduler.
+
+Acceptance values from the reference SPEC.
+"""
+
+from __future__ import annotations
+
+import json
+import random
+import threading
+
+import pytest
+
+from conftest import SETS
+
+from paper_2512_23969_b200 import batchgraph as bg
+from paper_2512_23969_b200 import tuner
+from paper_2512_23969_b200.config import TuningConfig
+from paper_2512_23969_b200.errors import ConfigError, FormatError, GraphExecutionError, TuningError, UsageError
+from paper_2512_23969_b200.params import derive
+
+
+def test_table3_reproduction():
+    r128 = tuner.tree_tune(tuner.TuneInput(derive("128f"))).best
+    assert (r128.lanes_per_set, r128.sets_fused, r128.lane_utilization, r128.scratch_utilization) == (704, 3, 0.6875,
+                                                                                                     0.6875)
+    r192 = tuner.tree_tune(tuner.TuneInput(derive("192f"))).best
+    assert (r192.lanes_per_set, r192.sets_fused, r192.lane_utilization, r192.scratch_utilization) == (768, 2, 0.75, 0.75)
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_candidates_feasible(set_id):
+    inp = tuner.TuneInput(derive(set_id), seme_per_block=232448)
+    res = tuner.tree_tune(inp)
+    assert res.candidates and all(tuner.is_feasible(c, inp) for c in res.candidates)
+    assert res.best == min(res.candidates, key=lambda c: c.sort_key(inp.params))
+
+
+def test_tune_infeasible():
+    with pytest.raises(TuningError):
+        tuner.tree_tune(tuner.TuneInput(derive("256f"), seme_per_block=1024))
+
+
+def test_padding_and_occupancy():
+    assert [(s.banks_per_access, s.lane_interval, s.rows_per_region) for s in map(tuner.padding_solve, (16, 24, 32))] \
+        == [(4, 8, 1), (6, 16, 3), (8, 4, 1)]
+    assert abs(tuner.occupancy(65536, 64, 1024, 48) - 2 / 3) < 1e-9
+    assert tuner.occupancy(65536, 128, 1024, 48) == 0
+    with pytest.raises(UsageError):
+        tuner.padding_solve(6)
+
+
+def test_select_backends_tie_rule():
+    runs = {}
+    for k in tuner.KERNELS:
+        for s in SETS:
+            runs[(k, s)] = {"baseline": [1.0] * 10, "tuned": [0.99] * 10}
+    runs[("TREE_Sign", "256f")]["tuned"] = [0.9] * 10
+    sel = tuner.select_backends(runs)
+    assert sel[("TREE_Sign", "256f")] == "tuned" and sel[("FORS_Sign", "128f")] == "baseline"
+    del runs[("WOTS_Sign", "192f")]
+    with pytest.raises(TuningError):
+        tuner.select_backends(runs)
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_device_candidates_respect_smem(set_id):
+    from paper_2512_23969_b200 import _lib
+
+    if not _lib.LIB_PATH.exists():
+        _lib.build_native()
+    cands = tuner.device_candidates(set_id, smem_optin=232448)
+    assert cands
+    p = derive(set_id)
+    for c in cands:
+        assert c.smem_bytes <= 232448 and c.lanes <= 1024
+        assert c.lanes == c.trees_per_set * (p.fors_t // 2 if c.relax else p.fors_t)
+    assert cands == sorted(cands, key=tuner.DeviceCandidate.key)
+
+
+def test_config_roundtrip(tmp_path):
+    cfg = TuningConfig.default()
+    cfg.validate()
+    path = tmp_path / "cfg.json"
+    cfg.save(path)
+    back = TuningConfig.load(path)
+    assert back.to_dict() == cfg.to_dict()
+    # reference-format file (no "b200" block) loads too
+    raw = json.loads(path.read_text())
+    for row in raw["sets"].values():
+        row.pop("b200")
+    path.write_text(json.dumps(raw))
+    ref = TuningConfig.load(path)
+    assert ref.sets["128f"].fusion.lanes_per_set == 704 and not ref.sets["128f"].b200
+    path.write_text("{")
+    with pytest.raises(FormatError):
+        TuningConfig.load(path)
+    bad = cfg.to_dict()
+    bad["sets"]["128f"]["b200"]["fors_trees_per_set"] = 40
+    with pytest.raises(ConfigError):
+        TuningConfig.from_dict(bad)
+
+
+class _FakeSigner:
+    """Stage bodies that record order; bytes depend only on the message."""
+
+    sig_bytes = 8
+
+    def __init__(self, fail_on=None):
+        self.fail_on = fail_on
+        self.order = []
+        self.lock = threading.Lock()
+
+    def prepare(self, msg, buffer):
+        return type("Plan", (), {"msg": msg, "buffer": buffer, "f": False, "t": False})()
+
+    def run_fors(self, plan):
+        with self.lock:
+            self.order.append(("F", plan.msg))
+        plan.f = True
+
+    def run_tree(self, plan):
+        if self.fail_on is not None and plan.msg == self.fail_on:
+            raise RuntimeError("boom")
+        with self.lock:
+            self.order.append(("T", plan.msg))
+        plan.t = True
+
+    def run_wots(self, plan):
+        assert plan.f and plan.t
+        plan.buffer[:] = (sum(plan.msg) & 0xFF).to_bytes(1, "big") * 8
+
+
+def test_execute_graphs_properties():
+    msgs = [bytes([i]) * 3 for i in range(12)]
+    base, _ = bg.execute_graphs(bg.build_graphs(msgs, 4, 3), 1, _FakeSigner())
+    seen_orders = set()
+    for trial in range(40):
+        graphs = bg.build_graphs(msgs, 4, 3)
+        pool = bg.BufferPool()
+        signer = _FakeSigner()
+        sigs, log = bg.execute_graphs(graphs, random.choice([2, 4, 8]), signer, pool=pool,
+                                      rng=random.Random(trial))
+        assert sigs == base
+        assert bg.replay_check(log, graphs)
+        assert pool.frozen and pool.allocations == len(msgs)
+        first = {}
+        for st, m in signer.order:
+            first.setdefault(m, st)
+        seen_orders |= set(first.values())
+    assert seen_orders == {"F", "T"}
+    with pytest.raises(ConfigError):
+        pool.alloc(1)
+    with pytest.raises(GraphExecutionError):
+        bg.execute_graphs(bg.build_graphs(msgs, 4, 3), 2, _FakeSigner(fail_on=msgs[5]))
+    with pytest.raises(UsageError):
+        bg.build_graphs(msgs, 2, 2)

@@ -55,19 +55,24 @@ __global__ void __launch_bounds__(NT) chain_kernel(uint32_t* out, int reps) {
 static uint32_t* g_ref = nullptr;
 
 template <class V, int ILP, int NT = 128>
-void run(const char* name) {
+void run(const char* name, int cap_blocks = 0) {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int blocks = sms * 64 / ILP, reps = 8;
   const size_t threads = (size_t)blocks * NT;
   uint32_t* out;
   cudaMalloc(&out, threads * ILP * 4 * 4);
-  chain_kernel<V, ILP, NT><<<blocks, NT>>>(out, 1);
+  size_t dyn = 0;
+  if (cap_blocks) {
+    dyn = (size_t)(200 * 1024) / cap_blocks;
+    cudaFuncSetAttribute(chain_kernel<V, ILP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  }
+  chain_kernel<V, ILP, NT><<<blocks, NT, dyn>>>(out, 1);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   cudaEventRecord(a);
-  chain_kernel<V, ILP, NT><<<blocks, NT>>>(out, reps);
+  chain_kernel<V, ILP, NT><<<blocks, NT, dyn>>>(out, reps);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
@@ -81,35 +86,28 @@ void run(const char* name) {
   if (!g_ref) {
     g_ref = h;
   } else if (ILP == 1) {
-    for (size_t i = 0; i < threads * 4; i++) bad += h[i] != g_ref[i];
+    for (size_t i = 0; i < (size_t)sms * 64 * 128 * 4 && i < threads * 4; i++) bad += h[i] != g_ref[i];
     free(h);
   } else {
     free(h);
   }
   cudaFuncAttributes fa;
   cudaFuncGetAttributes(&fa, chain_kernel<V, ILP, NT>);
-  printf("%-34s ILP=%d regs=%3d  %8.3f Gcomp/s  (%.2f ms)  %s%s\n", name, ILP, fa.numRegs, comps / ms / 1e6, ms,
+  printf("%-34s cap=%d ILP=%d regs=%3d  %8.3f Gcomp/s  (%.2f ms)  %s%s\n", name, cap_blocks, ILP, fa.numRegs, comps / ms / 1e6, ms,
          bad ? "MISMATCH " : "", e != cudaSuccess ? cudaGetErrorString(e) : "");
   cudaFree(out);
 }
 
 int main() {
+  setvbuf(stdout, NULL, _IONBF, 0);
   run<Native, 1>("Native");
-  run<Imad, 1>("Imad");
-  run<Mix<0, 0, 0, true, false>, 1>("Mix<0,0,0,shr,->");
-  run<Mix<0, 0, 0, true, true>, 1>("Mix<0,0,0,shr,eadd>");
-  run<Mix<1, 0, 0, true, true>, 1>("Mix<1,0,0,shr,eadd>");
-  run<Mix<1, 1, 0, true, true>, 1>("Mix<1,1,0,shr,eadd>");
-  run<Mix<1, 1, 1, true, true>, 1>("Mix<1,1,1,shr,eadd>");
-  run<Mix<2, 1, 1, true, true>, 1>("Mix<2,1,1,shr,eadd>");
-  run<Mix<2, 2, 1, true, true>, 1>("Mix<2,2,1,shr,eadd>");
-  run<Mix<1, 1, 0, true, false>, 1>("Mix<1,1,0,shr,->");
-  run<Mix<1, 0, 1, true, true>, 1>("Mix<1,0,1,shr,eadd>");
-  run<Native, 2>("Native");
-  run<Mix<1, 1, 0, true, true>, 2>("Mix<1,1,0,shr,eadd>");
-  run<Mix<1, 1, 1, true, true>, 2>("Mix<1,1,1,shr,eadd>");
-  run<Mix<2, 1, 1, true, true>, 2>("Mix<2,1,1,shr,eadd>");
-  run<Native, 1, 256>("Native NT256");
-  run<Mix<1, 1, 0, true, true>, 1, 256>("Mix<1,1,0,shr,eadd> NT256");
+  //           NS1 NS0 NSS SHR T1F ANF WF
+  run<Mix<0, 0, 0, true, 1, true, false>, 1>("Mix 000S1A- (Fast)");
+  run<Mix<0, 0, 0, true, 3, true, false>, 1>("Mix 000S3A-");
+  run<Mix<0, 0, 0, true, 3, true, true>, 1>("Mix 000S3AW");
+  run<Mix<1, 0, 0, true, 3, true, false>, 1>("Mix 100S3A-");
+  run<Mix<0, 1, 0, true, 3, true, false>, 1>("Mix 010S3A-");
+  run<Mix<0, 0, 0, false, 3, true, false>, 1>("Mix 000-3A-");
+  run<Mix<0, 0, 0, true, 3, false, false>, 1>("Mix 000S3--");
   return 0;
 }
