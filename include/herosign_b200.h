@@ -67,6 +67,8 @@ typedef struct {
   int32_t wots_from_tree;     /* 1: TREE_Sign records the signing leaf's
                                  chains and WOTS_Sign gathers them; 0: WOTS_Sign
                                  recomputes its chains (reference shape)     */
+  int32_t streams;            /* T: concurrent sub-batch graphs per batch
+                                 (paper's multi-stream batching), 1..8       */
 } hs_set_config;
 
 HS_API int hs_open(int device, hs_t **out);

@@ -44,6 +44,7 @@ class SetConfig(ctypes.Structure):
         ("use_graph", ctypes.c_int32),
         ("chunk", ctypes.c_int32),
         ("wots_from_tree", ctypes.c_int32),
+        ("streams", ctypes.c_int32),
     ]
 
 

@@ -27,8 +27,8 @@ MAX_LANES = 1024
 # Engine defaults (csrc/hs_api.cu default_config); tune_on_device refines them.
 B200_DEFAULTS = {
     "128f": {"fors_trees_per_set": 11, "fors_sets_fused": 3, "fors_relax": False},
-    "192f": {"fors_trees_per_set": 3, "fors_sets_fused": 3, "fors_relax": False},
-    "256f": {"fors_trees_per_set": 2, "fors_sets_fused": 2, "fors_relax": True},
+    "192f": {"fors_trees_per_set": 3, "fors_sets_fused": 8, "fors_relax": False},
+    "256f": {"fors_trees_per_set": 3, "fors_sets_fused": 6, "fors_relax": True},
 }
 
 
@@ -57,7 +57,7 @@ class TuningConfig:
             backends = {"FORS_Sign": "tuned", "TREE_Sign": "tuned" if tuned_all else "baseline",
                         "WOTS_Sign": "tuned" if tuned_all else "baseline"}
             b200 = dict(B200_DEFAULTS[set_id])
-            b200.update({"variant": {k: 0 for k in KERNELS}, "wots_from_tree": True, "chunk": 16384})
+            b200.update({"variant": {k: 0 for k in KERNELS}, "wots_from_tree": True, "chunk": 16384, "streams": 2})
             sets[set_id] = SetConfig(best, padding_solve(p.n), backends, set_id == "256f", b200)
         return cls(seme_per_block=seme, sets=sets)
 
@@ -94,7 +94,7 @@ class TuningConfig:
         for set_id, cfg in self.sets.items():
             b = dict(cfg.b200) if cfg.b200 else {}
             kw = {}
-            for key in ("fors_trees_per_set", "fors_sets_fused", "fors_relax", "wots_from_tree", "chunk"):
+            for key in ("fors_trees_per_set", "fors_sets_fused", "fors_relax", "wots_from_tree", "chunk", "streams"):
                 if key in b:
                     kw[key] = b[key]
             if "variant" in b:
@@ -111,7 +111,7 @@ class TuningConfig:
             cfg.sets[set_id].b200 = {
                 "fors_trees_per_set": e["fors_trees_per_set"], "fors_sets_fused": e["fors_sets_fused"],
                 "fors_relax": e["fors_relax"], "variant": {k: e["variant"][k] for k in KERNELS},
-                "wots_from_tree": e["wots_from_tree"], "chunk": e["chunk"],
+                "wots_from_tree": e["wots_from_tree"], "chunk": e["chunk"], "streams": e["streams"],
             }
             cfg.sets[set_id].backends = {k: "tuned" if e["variant"][k] else "baseline" for k in KERNELS}
         return cfg

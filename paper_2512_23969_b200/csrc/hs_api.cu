@@ -71,14 +71,17 @@ hs_set_config default_config(int set) {
   hs_set_config c;
   std::memset(&c, 0, sizeof c);
   // Defaults from the on-device Tree Tuning search (python tuner); see DESIGN.md.
-  static const int nt[3] = {11, 3, 2}, ff[3] = {3, 3, 2}, rx[3] = {0, 0, 1};
+  // (b200_tuned.json, written by tools/tune_all.py on a B200, overrides these.)
+  static const int nt[3] = {11, 3, 3}, ff[3] = {3, 8, 6}, rx[3] = {0, 0, 1};
+  static const int var[3][4] = {{1, 1, 0, 0}, {0, 1, 0, 0}, {0, 0, 0, 0}};
   c.fors_trees_per_set = nt[set];
   c.fors_sets_fused = ff[set];
   c.fors_relax = rx[set];
-  for (int i = 0; i < 4; i++) c.variant[i] = 0;
+  for (int i = 0; i < 4; i++) c.variant[i] = var[set][i];
   c.use_graph = 1;
   c.chunk = 16384;
   c.wots_from_tree = 1;
+  c.streams = 2;
   return c;
 }
 
@@ -136,6 +139,8 @@ struct SetState {
 
 using GraphKey = std::tuple<int, uint32_t, int, int, uint64_t, std::string>;
 
+constexpr int kMaxStreams = 8;
+
 }  // namespace
 
 struct hs_ctx {
@@ -153,6 +158,8 @@ struct hs_ctx {
   int sm_count = 0, smem_optin = 0, cc_major = 0, cc_minor = 0;
   void* flush = nullptr;
   size_t flush_cap = 0;
+  cudaStream_t ls[kMaxStreams] = {};   // sub-batch launch streams
+  cudaEvent_t staged = nullptr, ls_done[kMaxStreams] = {};
 };
 
 namespace {
@@ -193,7 +200,8 @@ int check_layout(hs_t* h, int set, const hs_set_config& c) {
   if (c.fors_trees_per_set < 1 || c.fors_sets_fused < 1)
     return fail(h, HS_E_CONFIG, "fusion counts must be positive");
   const int lanes = c.fors_trees_per_set * (c.fors_relax ? I.t / 2 : I.t);
-  if (lanes > 1024) return fail(h, HS_E_CONFIG, "layout needs %d lanes; blocks hold at most 1024", lanes);
+  if (lanes > kForsMaxLanes)
+    return fail(h, HS_E_CONFIG, "layout needs %d lanes; FORS_Sign blocks hold at most %d", lanes, kForsMaxLanes);
   if (c.fors_trees_per_set * c.fors_sets_fused > I.k)
     return fail(h, HS_E_CONFIG, "layout holds more than k=%d trees per CTA", I.k);
   size_t smem = fors_smem(set, c.fors_trees_per_set, c.fors_sets_fused, c.fors_relax);
@@ -203,6 +211,7 @@ int check_layout(hs_t* h, int set, const hs_set_config& c) {
     if (c.variant[i] != 0 && c.variant[i] != 1) return fail(h, HS_E_CONFIG, "variant must be 0 or 1");
   if (c.chunk < 1) return fail(h, HS_E_CONFIG, "chunk must be >= 1");
   if (c.wots_from_tree != 0 && c.wots_from_tree != 1) return fail(h, HS_E_CONFIG, "wots_from_tree must be 0 or 1");
+  if (c.streams < 1 || c.streams > kMaxStreams) return fail(h, HS_E_CONFIG, "streams must be in 1..%d", kMaxStreams);
   return HS_OK;
 }
 
@@ -228,7 +237,11 @@ int ensure_capacity(hs_t* h, int set, uint32_t count, size_t msg_bytes) {
   return HS_OK;
 }
 
-LaunchArgs make_args(hs_t* h, int set, uint32_t count) {
+// Arguments for messages [first, first + count) of the staged batch.  Message
+// offsets stay absolute into the staged blob; every per-message buffer is
+// offset by `first`, so sub-batches are independent launches.
+LaunchArgs make_args(hs_t* h, int set, uint32_t first, uint32_t count) {
+  const SetInfo& I = kInfo[set];
   SetState& St = h->sets[set];
   Buffers& B = h->buf[set];
   LaunchArgs a;
@@ -236,19 +249,22 @@ LaunchArgs make_args(hs_t* h, int set, uint32_t count) {
   a.keys = St.keys;
   a.nkeys = St.nkeys;
   a.msgs = B.msgs;
-  a.offs = B.offs;
-  a.key_idx = St.has_keyidx ? B.keyidx : nullptr;
-  a.opt_rand = St.has_optrand ? B.optrand : nullptr;
+  a.offs = B.offs + first;
+  a.key_idx = St.has_keyidx ? B.keyidx + first : nullptr;
+  a.opt_rand = St.has_optrand ? B.optrand + (size_t)first * I.n : nullptr;
   a.count = count;
-  a.sigs = B.sigs;
-  a.plans = B.plans;
-  a.indices = B.idx;
-  a.roots = B.roots;
-  a.fors_roots = B.froots;
+  a.sigs = B.sigs + (size_t)first * I.sig_bytes;
+  a.plans = B.plans + first;
+  a.indices = B.idx + (size_t)first * I.k;
+  a.roots = B.roots + (size_t)first * (I.d + 1) * 8;
+  a.fors_roots = B.froots + (size_t)first * I.k * 8;
   a.fors_trees_per_set = St.cfg.fors_trees_per_set;
   a.fors_sets_fused = St.cfg.fors_sets_fused;
   a.fors_relax = St.cfg.fors_relax;
-  a.stash = (St.cfg.wots_from_tree && B.stash && B.stash_cap >= (size_t)count * stash_words(set)) ? B.stash : nullptr;
+  const size_t sw = stash_words(set);
+  a.stash = (St.cfg.wots_from_tree && B.stash && B.stash_cap >= ((size_t)first + count) * sw)
+                ? B.stash + (size_t)first * sw
+                : nullptr;
   return a;
 }
 
@@ -292,16 +308,15 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
   return cudaSuccess;
 }
 
-int run_batch(hs_t* h, int set, uint32_t count, int mode) {
+// One sub-batch as a CUDA graph (captured once per shape and offset) or as
+// plain stream launches.  The graph is launched on `launch_stream`.
+int run_one(hs_t* h, int set, uint32_t first, uint32_t count, int mode, cudaStream_t launch_stream) {
   SetState& St = h->sets[set];
-  if (count == 0) return HS_OK;
-  const LaunchArgs a = make_args(h, set, count);
+  const LaunchArgs a = make_args(h, set, first, count);
   const bool serial = mode == 1;
-  h->last_set = set;
-  h->last_mode = mode;
   if (!serial && St.cfg.use_graph) {
     GraphKey key{set, count, St.has_keyidx ? 1 : 0, St.has_optrand ? 1 : 0, h->buf[set].gen,
-                 cfg_fingerprint(St.cfg) + "/" + std::to_string((uintptr_t)St.keys)};
+                 cfg_fingerprint(St.cfg) + "/" + std::to_string((uintptr_t)St.keys) + "/" + std::to_string(first)};
     auto it = h->graphs.find(key);
     if (it == h->graphs.end()) {
       cudaGraph_t g;
@@ -316,10 +331,48 @@ int run_batch(hs_t* h, int set, uint32_t count, int mode) {
       h->launches -= 5;  // capture does not launch
       it = h->graphs.emplace(key, ex).first;
     }
-    CUDA_TRY(h, cudaGraphLaunch(it->second, h->s0));
+    CUDA_TRY(h, cudaGraphLaunch(it->second, launch_stream));
     h->launches += 5;
   } else {
     CUDA_TRY(h, enqueue(h, set, a, false, serial));
+  }
+  return HS_OK;
+}
+
+// Sub-batch split: T = cfg.streams graphs on T launch streams run
+// concurrently (the paper's m x T multi-stream batching),
+// so one graph's FORS/TREE tail overlaps the others' bulk.  `fetch_to`
+// (optional, pinned host memory) receives each sub-batch's signatures from
+// its own stream as soon as it is done, overlapping D2H with compute.
+int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nullptr) {
+  if (count == 0) return HS_OK;
+  h->last_set = set;
+  h->last_mode = mode;
+  const size_t sb = (size_t)kInfo[set].sig_bytes;
+  int T = std::max(1, std::min(h->sets[set].cfg.streams, kMaxStreams));
+  if (mode == 1 || !h->sets[set].cfg.use_graph) T = 1;
+  T = (int)std::min<uint32_t>((uint32_t)T, std::max<uint32_t>(1u, count / 64u));
+  if (T == 1) {
+    int rc = run_one(h, set, 0, count, mode, h->s0);
+    if (rc) return rc;
+    if (fetch_to)
+      CUDA_TRY(h, cudaMemcpyAsync(fetch_to, h->buf[set].sigs, count * sb, cudaMemcpyDeviceToHost, h->s0));
+    return HS_OK;
+  }
+  CUDA_TRY(h, cudaEventRecord(h->staged, h->s0));
+  const uint32_t per = (count + T - 1) / T;
+  for (int j = 0; j < T; j++) {
+    const uint32_t first = (uint32_t)j * per;
+    if (first >= count) break;
+    const uint32_t cn = std::min(per, count - first);
+    CUDA_TRY(h, cudaStreamWaitEvent(h->ls[j], h->staged, 0));
+    int rc = run_one(h, set, first, cn, mode, h->ls[j]);
+    if (rc) return rc;
+    if (fetch_to)
+      CUDA_TRY(h, cudaMemcpyAsync(fetch_to + first * sb, h->buf[set].sigs + first * sb, cn * sb,
+                                  cudaMemcpyDeviceToHost, h->ls[j]));
+    CUDA_TRY(h, cudaEventRecord(h->ls_done[j], h->ls[j]));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->s0, h->ls_done[j], 0));
   }
   return HS_OK;
 }
@@ -391,6 +444,11 @@ int hs_open(int device, hs_t** out) {
     return HS_E_CUDA;
   }
   for (auto& ev : h->ev) cudaEventCreate(&ev);
+  for (int j = 0; j < kMaxStreams; j++) {
+    cudaStreamCreateWithFlags(&h->ls[j], cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&h->ls_done[j], cudaEventDisableTiming);
+  }
+  cudaEventCreateWithFlags(&h->staged, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->join, cudaEventDisableTiming);
   for (int s = 0; s < 3; s++) h->sets[s].cfg = default_config(s);
@@ -412,6 +470,11 @@ void hs_close(hs_t* h) {
     cudaFree(h->sets[s].sk_raw);
   }
   if (h->flush) cudaFree(h->flush);
+  for (int j = 0; j < kMaxStreams; j++) {
+    cudaStreamDestroy(h->ls[j]);
+    cudaEventDestroy(h->ls_done[j]);
+  }
+  cudaEventDestroy(h->staged);
   for (auto& ev : h->ev) cudaEventDestroy(ev);
   cudaEventDestroy(h->fork);
   cudaEventDestroy(h->join);
@@ -569,17 +632,11 @@ int hs_sign_batch(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, c
     const uint32_t cn = std::min(chunk, count - first);
     int rc = stage_inputs(h, set, msgs, offs, key_idx, opt_rand, first, cn);
     if (rc) return rc;
-    rc = run_batch(h, set, cn, 0);
+    if (!direct) CUDA_TRY(h, grow_host(B.h_sigs, B.h_sigs_cap, (size_t)cn * sb));
+    rc = run_batch(h, set, cn, 0, direct ? sigs + first * sb : B.h_sigs);
     if (rc) return rc;
-    if (direct) {
-      CUDA_TRY(h, cudaMemcpyAsync(sigs + first * sb, B.sigs, cn * sb, cudaMemcpyDeviceToHost, h->s0));
-      CUDA_TRY(h, cudaStreamSynchronize(h->s0));
-    } else {
-      CUDA_TRY(h, grow_host(B.h_sigs, B.h_sigs_cap, (size_t)cn * sb));
-      CUDA_TRY(h, cudaMemcpyAsync(B.h_sigs, B.sigs, cn * sb, cudaMemcpyDeviceToHost, h->s0));
-      CUDA_TRY(h, cudaStreamSynchronize(h->s0));
-      std::memcpy(sigs + first * sb, B.h_sigs, cn * sb);
-    }
+    CUDA_TRY(h, cudaStreamSynchronize(h->s0));
+    if (!direct) std::memcpy(sigs + first * sb, B.h_sigs, cn * sb);
     float ms[5];
     if (hs_timings(h, ms, 5) == 5) {
       total_ms += ms[0];

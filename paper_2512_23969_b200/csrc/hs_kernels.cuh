@@ -237,9 +237,14 @@ __device__ __forceinline__ void wots_leaf(const KeyDev& K, uint32_t layer, uint6
 // consecutive lanes of one warp and are reduced with shuffles.
 // ---------------------------------------------------------------------------
 constexpr int kTreeBlock = 128;
+#ifndef HS_TREE_MIN_BLOCKS
+#define HS_TREE_MIN_BLOCKS 5
+#endif
+// 5 blocks -> <= 96 registers, 20 warps / SM; 256f (8-word nodes) uses 4 blocks / 128 registers
+constexpr int kTreeMinBlocks = HS_TREE_MIN_BLOCKS;
 
 template <int S, class V>
-__global__ void __launch_bounds__(kTreeBlock) tree_sign_kernel(LaunchArgs a) {
+__global__ void __launch_bounds__(kTreeBlock, (S == 2 ? 4 : kTreeMinBlocks)) tree_sign_kernel(LaunchArgs a) {
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
   __shared__ uint32_t tbuf[32 * kTreeBlock];
@@ -300,6 +305,9 @@ __global__ void __launch_bounds__(kTreeBlock) tree_sign_kernel(LaunchArgs a) {
 // level; each level's nodes of all fused trees are spread over every lane,
 // so one barrier covers all F sets.
 // ---------------------------------------------------------------------------
+// 768 lanes keep the register budget at 85 per thread (65536 / 768).
+constexpr int kForsMaxLanes = 768;
+
 template <int S>
 __host__ __device__ constexpr int fors_smem_words_per_tree(bool relax) {
   // region A (t or t/4 nodes) + region B (t/2 nodes)
@@ -317,7 +325,7 @@ __device__ __forceinline__ void fors_leaf(const uint32_t mid[8], const uint32_t*
 }
 
 template <int S, class V>
-__global__ void __launch_bounds__(1024) fors_sign_kernel(LaunchArgs a) {
+__global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) {
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
   constexpr int t = Pr::t;
@@ -335,8 +343,12 @@ __global__ void __launch_bounds__(1024) fors_sign_kernel(LaunchArgs a) {
   if (msg >= a.count) return;
   const int lanes_per_tree = relax ? t / 2 : t;
   const int capA = relax ? t / 4 : t;
-  uint32_t* regA = sm;                                 // [tpc][capA][NW]
-  uint32_t* regB = sm + (size_t)tpc * capA * NW;       // [tpc][t/2][NW]
+  // word-major (SoA) regions: word w of node (tree slot tl, index j) lives at
+  // X[w * S_X + tl * cap_X + j], so a lane's two children are one 8-byte
+  // shared load per word and a warp's accesses are bank-conflict free
+  const int SA = tpc * capA, SB = tpc * (t / 2);
+  uint32_t* regA = sm;                                 // [NW][tpc][capA]
+  uint32_t* regB = sm + (size_t)NW * SA;               // [NW][tpc][t/2]
 
   const MsgPlan pl = a.plans[msg];
   const KeyDev& K = a.keys[pl.key];
@@ -364,9 +376,9 @@ __global__ void __launch_bounds__(1024) fors_sign_kernel(LaunchArgs a) {
       uint32_t sk[8], lf[8];
       fors_leaf<S, V>(mid, sks, fa, (uint32_t)(g * t + lane_leaf), sk, lf);
       if ((uint32_t)lane_leaf == sel) store_node<NW>(fsig + g * tree_sig, sk);
-      uint32_t* dst = regA + ((size_t)tl * capA + lane_leaf) * NW;
+      uint32_t* dst = regA + (size_t)tl * capA + lane_leaf;
 #pragma unroll
-      for (int j = 0; j < NW; j++) dst[j] = lf[j];
+      for (int j = 0; j < NW; j++) dst[(size_t)j * SA] = lf[j];
     } else {
       uint32_t sk0[8], l0[8], sk1[8], l1[8];
       const uint32_t j2 = 2u * lane_leaf;
@@ -380,9 +392,9 @@ __global__ void __launch_bounds__(1024) fors_sign_kernel(LaunchArgs a) {
       for (int j = 0; j < NW; j++) { m[j] = l0[j]; m[NW + j] = l1[j]; }
       adrs_set_chain_hash(fa, 1, (uint32_t)lane_leaf + ((uint32_t)(g * t) >> 1));
       thash_reg<V, 2 * NW>(par, mid, fa, m);
-      uint32_t* dst = regB + ((size_t)tl * (t / 2) + lane_leaf) * NW;
+      uint32_t* dst = regB + (size_t)tl * (t / 2) + lane_leaf;
 #pragma unroll
-      for (int j = 0; j < NW; j++) dst[j] = par[j];
+      for (int j = 0; j < NW; j++) dst[(size_t)j * SB] = par[j];
     }
   }
   __syncthreads();
@@ -397,6 +409,8 @@ __global__ void __launch_bounds__(1024) fors_sign_kernel(LaunchArgs a) {
     uint32_t* dst = src_is_A ? regB : regA;
     const int src_cap = src_is_A ? capA : t / 2;
     const int dst_cap = src_is_A ? t / 2 : capA;
+    const int src_S = src_is_A ? SA : SB;
+    const int dst_S = src_is_A ? SB : SA;
     const int per_tree = t >> lvl;
     const int total = ntr * per_tree;
 #pragma unroll 1
@@ -404,10 +418,14 @@ __global__ void __launch_bounds__(1024) fors_sign_kernel(LaunchArgs a) {
       const int tl = q / per_tree;
       const int j = q % per_tree;
       const int g = g0 + tl;
-      const uint32_t* c = src + ((size_t)tl * src_cap + 2 * j) * NW;
+      const uint32_t* c = src + (size_t)tl * src_cap + 2 * j;
       uint32_t m[2 * NW];
 #pragma unroll
-      for (int w = 0; w < 2 * NW; w++) m[w] = c[w];
+      for (int w = 0; w < NW; w++) {
+        const uint2 v = *reinterpret_cast<const uint2*>(c + (size_t)w * src_S);
+        m[w] = v.x;
+        m[NW + w] = v.y;
+      }
       const uint32_t sel = (uint32_t)idx[g] >> (lvl - 1);
       if ((sel >> 1) == (uint32_t)j)
         store_node<NW>(fsig + g * tree_sig + Pr::n + (lvl - 1) * Pr::n, (sel & 1u) ? m : m + NW);
@@ -420,9 +438,9 @@ __global__ void __launch_bounds__(1024) fors_sign_kernel(LaunchArgs a) {
 #pragma unroll
         for (int w = 0; w < NW; w++) r[w] = par[w];
       } else {
-        uint32_t* d = dst + ((size_t)tl * dst_cap + j) * NW;
+        uint32_t* d = dst + (size_t)tl * dst_cap + j;
 #pragma unroll
-        for (int w = 0; w < NW; w++) d[w] = par[w];
+        for (int w = 0; w < NW; w++) d[(size_t)w * dst_S] = par[w];
       }
     }
     __syncthreads();

@@ -89,6 +89,7 @@ class Engine:
             "use_graph": bool(c.use_graph),
             "chunk": c.chunk,
             "wots_from_tree": bool(c.wots_from_tree),
+            "streams": c.streams,
         }
 
     def set_config(self, set_id: str, **kw) -> dict:
@@ -105,6 +106,7 @@ class Engine:
         c.use_graph = int(bool(cur["use_graph"]))
         c.chunk = int(cur["chunk"])
         c.wots_from_tree = int(bool(cur["wots_from_tree"]))
+        c.streams = int(cur["streams"])
         self._check(_lib.lib().hs_config_set(self._h, SET_INDEX[set_id], ctypes.byref(c)), "hs_config_set")
         return self.config(set_id)
 

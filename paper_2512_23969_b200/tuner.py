@@ -28,6 +28,7 @@ from .params import PARAMETER_SETS, DerivedParams, derive
 
 DEFAULT_SEME = 49152
 DEFAULT_T_MAX = 1024
+B200_FORS_MAX_LANES = 768  # csrc kForsMaxLanes: keeps 85 registers per lane
 DEFAULT_ALPHA = 0.5
 BANKS = 32
 BANK_WIDTH = 4
@@ -191,7 +192,7 @@ class DeviceCandidate:
         return (self.sync_score, -self.lane_utilization, -self.smem_utilization, self.lanes, self.sets_fused)
 
 
-def device_candidates(params, smem_optin: int, t_max: int = DEFAULT_T_MAX, alpha: float = DEFAULT_ALPHA,
+def device_candidates(params, smem_optin: int, t_max: int = B200_FORS_MAX_LANES, alpha: float = DEFAULT_ALPHA,
                       smem_of=None) -> list[DeviceCandidate]:
     """Algorithm 1 over (N_tree, F, Relax) with the B200 kernel's smem formula.
 
@@ -292,5 +293,14 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
             variants[kernel] = 1 if cell["imad"] < cell["native"] * (1.0 - tie_tolerance) else 0
             vtable[kernel] = cell
         engine.set_config(set_id, variant=variants)
+    # 3. multi-stream batching: T concurrent sub-batch graphs (whole-batch device time)
+    stable = {}
+    for T in (1, 2, 4):
+        engine.set_config(set_id, streams=T)
+        engine.bench_run(set_id, count, 1, 0, 0)
+        stable[T] = _trimmed_mean(engine.bench_run(set_id, count, reps, 0, 0))
+    best_T = min(stable, key=stable.get)
+    engine.set_config(set_id, streams=best_T)
     return {"set": set_id, "count": count, "smem_optin": info["smem_optin"], "layouts": table,
-            "best_layout": best, "variants": variants, "variant_ms": vtable, "config": engine.config(set_id)}
+            "best_layout": best, "variants": variants, "variant_ms": vtable, "streams_ms": stable,
+            "config": engine.config(set_id)}

@@ -91,7 +91,7 @@ def test_layouts_and_variants(eng, oracle_mod, set_id, variant, stash):
     base = eng.config(set_id)
     layouts = {"128f": [(1, 1, 0), (11, 3, 0), (2, 5, 1), (16, 2, 1)],
                "192f": [(1, 1, 0), (3, 3, 0), (4, 2, 1), (2, 5, 1)],
-               "256f": [(1, 1, 0), (2, 2, 1), (1, 5, 1), (4, 1, 1)]}[set_id]
+               "256f": [(1, 1, 0), (2, 2, 1), (1, 5, 1), (3, 6, 1)]}[set_id]
     try:
         for nt, f, rx in layouts:
             eng.set_config(set_id, fors_trees_per_set=nt, fors_sets_fused=f, fors_relax=bool(rx), wots_from_tree=stash,
@@ -144,17 +144,30 @@ def test_errors(eng):
     with pytest.raises(hs.UsageError):
         hs.sign_batch([b"a", b"b"], [sk], p, key_idx=[0, 3])
     with pytest.raises(hs.ConfigError):
-        eng.set_config("128f", fors_trees_per_set=17, fors_sets_fused=1)  # 1088 lanes
+        eng.set_config("128f", fors_trees_per_set=13, fors_sets_fused=1)  # 832 lanes > 768
 
 
-def test_config2_full_batch_128f(eng, oracle_mod):
-    """BASELINE config 2: 4096 messages, one key, every signature checked vs the CPU oracle."""
+@pytest.fixture(scope="module")
+def config2(oracle_mod):
     p = derive("128f")
     rng = random.Random(2512_23969)
     sk = oracle_mod.keygen("128f", rng.randbytes(3 * p.n))
     msgs = [rng.randbytes(32) for _ in range(4096)]
-    eng.upload_keys("128f", sk)
-    sigs = eng.sign_batch("128f", msgs)
     ref, _ = oracle_mod.sign_many("128f", sk, None, msgs)
+    return sk, msgs, ref
+
+
+@pytest.mark.parametrize("streams", [1, 3])
+def test_config2_full_batch_128f(eng, config2, streams):
+    """BASELINE config 2: 4096 messages, one key, every signature checked vs the
+    CPU oracle; streams=3 splits the batch into uneven concurrent sub-graphs."""
+    sk, msgs, ref = config2
+    eng.upload_keys("128f", sk)
+    base = eng.config("128f")
+    try:
+        eng.set_config("128f", streams=streams)
+        sigs = eng.sign_batch("128f", msgs)
+    finally:
+        eng.set_config("128f", **base)
     assert sigs == ref
     assert all(eng.verify_batch("128f", sk[32:], msgs, sigs))

@@ -73,7 +73,7 @@ def test_device_candidates_respect_smem(set_id):
     assert cands
     p = derive(set_id)
     for c in cands:
-        assert c.smem_bytes <= 232448 and c.lanes <= 1024
+        assert c.smem_bytes <= 232448 and c.lanes <= 768
         assert c.lanes == c.trees_per_set * (p.fors_t // 2 if c.relax else p.fors_t)
     assert cands == sorted(cands, key=tuner.DeviceCandidate.key)
 

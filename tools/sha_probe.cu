@@ -8,9 +8,8 @@
 
 using namespace hs;
 
-template <class V, int ILP, int NT>
+template <class V, int ILP, int NT, int NW>
 __global__ void __launch_bounds__(NT) chain_kernel(uint32_t* out, int reps) {
-  constexpr int NW = 4;
   uint32_t mid[8];
   for (int i = 0; i < 8; i++) mid[i] = 0x6a09e667u * (i + 1);
   uint32_t x[ILP][NW];
@@ -54,25 +53,25 @@ __global__ void __launch_bounds__(NT) chain_kernel(uint32_t* out, int reps) {
 
 static uint32_t* g_ref = nullptr;
 
-template <class V, int ILP, int NT = 128>
+template <class V, int ILP, int NT = 128, int NW = 4>
 void run(const char* name, int cap_blocks = 0) {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int blocks = sms * 64 / ILP, reps = 8;
   const size_t threads = (size_t)blocks * NT;
   uint32_t* out;
-  cudaMalloc(&out, threads * ILP * 4 * 4);
+  cudaMalloc(&out, threads * ILP * NW * 4);
   size_t dyn = 0;
   if (cap_blocks) {
     dyn = (size_t)(200 * 1024) / cap_blocks;
-    cudaFuncSetAttribute(chain_kernel<V, ILP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    cudaFuncSetAttribute(chain_kernel<V, ILP, NT, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   }
-  chain_kernel<V, ILP, NT><<<blocks, NT, dyn>>>(out, 1);
+  chain_kernel<V, ILP, NT, NW><<<blocks, NT, dyn>>>(out, 1);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   cudaEventRecord(a);
-  chain_kernel<V, ILP, NT><<<blocks, NT, dyn>>>(out, reps);
+  chain_kernel<V, ILP, NT, NW><<<blocks, NT, dyn>>>(out, reps);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
@@ -80,20 +79,20 @@ void run(const char* name, int cap_blocks = 0) {
   cudaError_t e = cudaGetLastError();
   double comps = (double)threads * ILP * reps * 15;
   // correctness vs Native ILP=1 on the first chain of each thread
-  uint32_t* h = (uint32_t*)malloc(threads * ILP * 16);
-  cudaMemcpy(h, out, threads * ILP * 16, cudaMemcpyDeviceToHost);
+  uint32_t* h = (uint32_t*)malloc(threads * ILP * NW * 4);
+  cudaMemcpy(h, out, threads * ILP * NW * 4, cudaMemcpyDeviceToHost);
   int bad = 0;
   if (!g_ref) {
     g_ref = h;
-  } else if (ILP == 1) {
+  } else if (ILP == 1 && NW == 4) {
     for (size_t i = 0; i < (size_t)sms * 64 * 128 * 4 && i < threads * 4; i++) bad += h[i] != g_ref[i];
     free(h);
   } else {
     free(h);
   }
   cudaFuncAttributes fa;
-  cudaFuncGetAttributes(&fa, chain_kernel<V, ILP, NT>);
-  printf("%-34s cap=%d ILP=%d regs=%3d  %8.3f Gcomp/s  (%.2f ms)  %s%s\n", name, cap_blocks, ILP, fa.numRegs, comps / ms / 1e6, ms,
+  cudaFuncGetAttributes(&fa, chain_kernel<V, ILP, NT, NW>);
+  printf("%-34s NW=%d cap=%d ILP=%d regs=%3d  %8.3f Gcomp/s  (%.2f ms)  %s%s\n", name, NW, cap_blocks, ILP, fa.numRegs, comps / ms / 1e6, ms,
          bad ? "MISMATCH " : "", e != cudaSuccess ? cudaGetErrorString(e) : "");
   cudaFree(out);
 }
@@ -109,5 +108,12 @@ int main() {
   run<Mix<0, 1, 0, true, 3, true, false>, 1>("Mix 010S3A-");
   run<Mix<0, 0, 0, false, 3, true, false>, 1>("Mix 000-3A-");
   run<Mix<0, 0, 0, true, 3, false, false>, 1>("Mix 000S3--");
+  run<Native, 1, 128, 8>("Native", 0);
+  run<Native, 1, 128, 8>("Native", 4);
+  run<Mix<0, 0, 0, true, 1, true, false>, 1, 128, 8>("Fast", 0);
+  run<Mix<0, 0, 0, true, 1, true, false>, 1, 128, 8>("Fast", 4);
+  run<Mix<0, 0, 0, true, 3, true, false>, 1, 128, 8>("Mix 000S3A-", 4);
+  run<Native, 1, 128, 6>("Native", 5);
+  run<Mix<0, 0, 0, true, 1, true, false>, 1, 128, 6>("Fast", 5);
   return 0;
 }
