@@ -1,0 +1,91 @@
+"""BASELINE config 5: mixed-key stress -- M messages across 1024 keypairs per set.
+
+    python tools/stress_c5.py [--messages 1048576] [--keys 1024] [--sets 128f,192f,256f]
+
+Keys come from GPU keygen (a sample is re-derived by the CPU oracle); message i
+is signed with key i mod 1024.  Every signature is
+verified by the GPU verifier, and at least one signature per key is compared
+byte-for-byte with the oracle.  Signing runs in chunks so host memory stays
+bounded; throughput is the signing time only (chunk staging + graph + D2H).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+
+import oracle  # noqa: E402  (checker)
+
+import paper_2512_23969_b200 as hs  # noqa: E402
+from paper_2512_23969_b200.engine import PinnedBuffer, pack_messages  # noqa: E402
+
+
+def run_set(eng, set_id: str, messages: int, nkeys: int, chunk: int) -> dict:
+    p = hs.derive(set_id)
+    rng = random.Random(2512_23969 + 5)
+    seeds = [rng.randbytes(3 * p.n) for _ in range(nkeys)]
+    t0 = time.perf_counter()
+    sks = eng.keygen_batch(set_id, seeds)
+    keygen_s = time.perf_counter() - t0
+    for i in range(0, nkeys, max(1, nkeys // 8)):
+        assert sks[i] == oracle.keygen(set_id, seeds[i]), f"keygen mismatch at key {i}"
+    eng.upload_keys(set_id, sks)
+    pks = b"".join(sk[2 * p.n:] for sk in sks)
+    out = PinnedBuffer(chunk * p.sig_bytes)
+    sign_s = 0.0
+    verified = 0
+    checked = 0
+    per_key_checked = set()
+    for c0 in range(0, messages, chunk):
+        cn = min(chunk, messages - c0)
+        msgs = [rng.randbytes(32) for _ in range(cn)]
+        kidx = np.array([(c0 + i) % nkeys for i in range(cn)], dtype=np.uint32)
+        blob, offs = pack_messages(msgs)
+        t0 = time.perf_counter()
+        eng.sign_into(set_id, blob, offs, cn, out.ptr, key_idx=kidx)
+        sign_s += time.perf_counter() - t0
+        raw = bytes(out.view[: cn * p.sig_bytes])
+        sigs = [raw[i * p.sig_bytes:(i + 1) * p.sig_bytes] for i in range(cn)]
+        ok = eng.verify_batch(set_id, pks, msgs, sigs, key_idx=kidx.tolist())
+        assert all(ok), f"GPU verify failed in chunk at {c0}"
+        verified += cn
+        # oracle check: first message of every key not yet checked in this chunk
+        todo = [i for i in range(cn) if int(kidx[i]) not in per_key_checked][: nkeys]
+        if todo:
+            ref, _ = oracle.sign_many(set_id, b"".join(sks), [int(kidx[i]) for i in todo], [msgs[i] for i in todo])
+            for i, r in zip(todo, ref):
+                assert sigs[i] == r, f"oracle mismatch at message {c0 + i}"
+                per_key_checked.add(int(kidx[i]))
+            checked += len(todo)
+    out.free()
+    return {"set": set_id, "messages": messages, "keys": nkeys, "sign_s": round(sign_s, 3),
+            "sig_per_s": round(messages / sign_s, 1), "keygen_s": round(keygen_s, 3), "verified": verified,
+            "oracle_checked": checked, "keys_checked": len(per_key_checked)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--messages", type=int, default=1 << 20)
+    ap.add_argument("--keys", type=int, default=1024)
+    ap.add_argument("--chunk", type=int, default=65536)
+    ap.add_argument("--sets", default="128f,192f,256f")
+    a = ap.parse_args()
+    oracle.build()
+    eng = hs.get_engine(int(os.environ.get("LOCAL_RANK", "0")))
+    for set_id in a.sets.split(","):
+        print(json.dumps(run_set(eng, set_id, a.messages, a.keys, a.chunk)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
