@@ -69,6 +69,10 @@ typedef struct {
                                  recomputes its chains (reference shape)     */
   int32_t streams;            /* T: concurrent sub-batch graphs per batch
                                  (paper's multi-stream batching), 1..8       */
+  int32_t shared_layers;      /* top hypertree layers whose subtrees are
+                                 computed once per (key, tree) per batch
+                                 instead of once per message (0 = off; max
+                                 3 for 128f/192f, 2 for 256f)                */
 } hs_set_config;
 
 HS_API int hs_open(int device, hs_t **out);

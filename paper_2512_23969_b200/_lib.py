@@ -45,6 +45,7 @@ class SetConfig(ctypes.Structure):
         ("chunk", ctypes.c_int32),
         ("wots_from_tree", ctypes.c_int32),
         ("streams", ctypes.c_int32),
+        ("shared_layers", ctypes.c_int32),
     ]
 
 

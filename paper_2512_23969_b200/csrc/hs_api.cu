@@ -49,6 +49,24 @@ cudaError_t launch(int set, int which, int variant, const LaunchArgs& a, cudaStr
   return cudaErrorInvalidValue;
 }
 
+size_t shared_words(int set, int layers) {
+  switch (set) {
+    case 0: return shared_words_per_key<0>(layers);
+    case 1: return shared_words_per_key<1>(layers);
+    case 2: return shared_words_per_key<2>(layers);
+  }
+  return 0;
+}
+
+int shared_max(int set) {
+  switch (set) {
+    case 0: return shared_max_layers<0>();
+    case 1: return shared_max_layers<1>();
+    case 2: return shared_max_layers<2>();
+  }
+  return 0;
+}
+
 size_t stash_words(int set) {
   switch (set) {
     case 0: return stash_words_per_msg<0>();
@@ -81,7 +99,8 @@ hs_set_config default_config(int set) {
   c.use_graph = 1;
   c.chunk = 16384;
   c.wots_from_tree = 1;
-  c.streams = 2;
+  c.streams = 1;
+  c.shared_layers = shared_max(set);
   return c;
 }
 
@@ -118,6 +137,8 @@ struct Buffers {
   uint32_t* roots = nullptr; size_t roots_cap = 0;
   uint32_t* froots = nullptr; size_t froots_cap = 0;
   uint32_t* stash = nullptr; size_t stash_cap = 0;
+  uint32_t* shared = nullptr; size_t shared_cap = 0;   // subtree-sharing table
+  uint8_t* key_used = nullptr; size_t key_used_cap = 0;
   // pinned staging
   uint8_t* h_msgs = nullptr; size_t h_msgs_cap = 0;
   uint64_t* h_offs = nullptr; size_t h_offs_cap = 0;
@@ -151,6 +172,8 @@ struct hs_ctx {
   SetState sets[3];
   Buffers buf[3];
   std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::map<GraphKey, int> graph_kernels;
+  int last_kernels = 5;
   std::string err;
   int64_t launches = 0;
   int last_set = -1;
@@ -185,14 +208,15 @@ bool valid_set(int set) { return set >= 0 && set <= 2; }
 
 std::string cfg_fingerprint(const hs_set_config& c) {
   char b[160];
-  snprintf(b, sizeof b, "%d/%d/%d/%d%d%d%d/%d", c.fors_trees_per_set, c.fors_sets_fused, c.fors_relax,
-           c.variant[0], c.variant[1], c.variant[2], c.variant[3], c.wots_from_tree);
+  snprintf(b, sizeof b, "%d/%d/%d/%d%d%d%d/%d/%d", c.fors_trees_per_set, c.fors_sets_fused, c.fors_relax,
+           c.variant[0], c.variant[1], c.variant[2], c.variant[3], c.wots_from_tree, c.shared_layers);
   return b;
 }
 
 void drop_graphs(hs_t* h) {
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
   h->graphs.clear();
+  h->graph_kernels.clear();
 }
 
 int check_layout(hs_t* h, int set, const hs_set_config& c) {
@@ -212,6 +236,8 @@ int check_layout(hs_t* h, int set, const hs_set_config& c) {
   if (c.chunk < 1) return fail(h, HS_E_CONFIG, "chunk must be >= 1");
   if (c.wots_from_tree != 0 && c.wots_from_tree != 1) return fail(h, HS_E_CONFIG, "wots_from_tree must be 0 or 1");
   if (c.streams < 1 || c.streams > kMaxStreams) return fail(h, HS_E_CONFIG, "streams must be in 1..%d", kMaxStreams);
+  if (c.shared_layers < 0 || c.shared_layers > shared_max(set))
+    return fail(h, HS_E_CONFIG, "shared_layers must be in 0..%d for this set", shared_max(set));
   return HS_OK;
 }
 
@@ -265,6 +291,14 @@ LaunchArgs make_args(hs_t* h, int set, uint32_t first, uint32_t count) {
   a.stash = (St.cfg.wots_from_tree && B.stash && B.stash_cap >= ((size_t)first + count) * sw)
                 ? B.stash + (size_t)first * sw
                 : nullptr;
+  // subtree sharing needs the stash (WOTS gather) and a table sized for the key set
+  const int L = St.cfg.shared_layers;
+  if (a.stash && L > 0 && B.shared && B.shared_cap >= (size_t)St.nkeys * shared_words(set, L) && B.key_used &&
+      B.key_used_cap >= St.nkeys) {
+    a.shared = B.shared;
+    a.shared_layers = L;
+    a.key_used = B.key_used;
+  }
   return a;
 }
 
@@ -277,7 +311,9 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
   };
   cudaError_t e;
 #define TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
+  const int kernels = 5 + (a.shared_layers > 0 ? 1 : 0);
   TRY(rec(0, h->s0));
+  if (a.shared_layers > 0) TRY(cudaMemsetAsync(a.key_used, 0, a.nkeys, h->s0));
   TRY(launch(set, K_PREP, c.variant[3], a, h->s0));
   TRY(rec(1, h->s0));
   if (serial) {
@@ -285,13 +321,18 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
     TRY(launch(set, K_FORSPK, c.variant[0], a, h->s0));
     TRY(rec(2, h->s0));
     TRY(launch(set, K_TREE, c.variant[1], a, h->s0));
-    TRY(rec(3, h->s0));
+    TRY(rec(3, h->s0));  // [2,3] = per-message TREE_Sign only (the roofline kernel)
+    if (a.shared_layers > 0) TRY(launch(set, K_TREE_SHARED, c.variant[1], a, h->s0));
     TRY(rec(5, h->s0));
     TRY(launch(set, a.stash ? K_WOTS_GATHER : K_WOTS, c.variant[2], a, h->s0));
     TRY(rec(4, h->s0));
   } else {
     TRY(cudaEventRecord(h->fork, h->s0));
     TRY(cudaStreamWaitEvent(h->s1, h->fork, 0));
+    // the shared-subtree kernel is small and latency bound (a few subtrees,
+    // one thread per leaf): start it first on the FORS branch so it runs
+    // under the per-message TREE_Sign instead of after it
+    if (a.shared_layers > 0) TRY(launch(set, K_TREE_SHARED, c.variant[1], a, h->s1));
     TRY(launch(set, K_FORS, c.variant[0], a, h->s1));
     TRY(launch(set, K_FORSPK, c.variant[0], a, h->s1));
     TRY(rec(2, h->s1));
@@ -304,7 +345,8 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
     TRY(rec(4, h->s0));
   }
 #undef TRY
-  h->launches += 5;
+  h->launches += kernels;
+  h->last_kernels = kernels;
   return cudaSuccess;
 }
 
@@ -316,7 +358,8 @@ int run_one(hs_t* h, int set, uint32_t first, uint32_t count, int mode, cudaStre
   const bool serial = mode == 1;
   if (!serial && St.cfg.use_graph) {
     GraphKey key{set, count, St.has_keyidx ? 1 : 0, St.has_optrand ? 1 : 0, h->buf[set].gen,
-                 cfg_fingerprint(St.cfg) + "/" + std::to_string((uintptr_t)St.keys) + "/" + std::to_string(first)};
+                 cfg_fingerprint(St.cfg) + "/" + std::to_string((uintptr_t)St.keys) + "/" + std::to_string(St.nkeys) +
+                     "/" + std::to_string(first)};
     auto it = h->graphs.find(key);
     if (it == h->graphs.end()) {
       cudaGraph_t g;
@@ -328,11 +371,12 @@ int run_one(hs_t* h, int set, uint32_t first, uint32_t count, int mode, cudaStre
       cudaGraphExec_t ex;
       CUDA_TRY(h, cudaGraphInstantiate(&ex, g, 0));
       cudaGraphDestroy(g);
-      h->launches -= 5;  // capture does not launch
+      h->launches -= h->last_kernels;  // capture does not launch
+      h->graph_kernels[key] = h->last_kernels;
       it = h->graphs.emplace(key, ex).first;
     }
     CUDA_TRY(h, cudaGraphLaunch(it->second, launch_stream));
-    h->launches += 5;
+    h->launches += h->graph_kernels[key];
   } else {
     CUDA_TRY(h, enqueue(h, set, a, false, serial));
   }
@@ -350,7 +394,8 @@ int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nu
   h->last_mode = mode;
   const size_t sb = (size_t)kInfo[set].sig_bytes;
   int T = std::max(1, std::min(h->sets[set].cfg.streams, kMaxStreams));
-  if (mode == 1 || !h->sets[set].cfg.use_graph) T = 1;
+  // sub-batches would race on the per-batch shared-subtree table
+  if (mode == 1 || !h->sets[set].cfg.use_graph || h->sets[set].cfg.shared_layers > 0) T = 1;
   T = (int)std::min<uint32_t>((uint32_t)T, std::max<uint32_t>(1u, count / 64u));
   if (T == 1) {
     int rc = run_one(h, set, 0, count, mode, h->s0);
@@ -404,6 +449,17 @@ int stage_inputs(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, co
   if (opt_rand)
     CUDA_TRY(h, cudaMemcpyAsync(B.optrand, opt_rand + (size_t)first * I.n, (size_t)count * I.n,
                                 cudaMemcpyHostToDevice, h->s0));
+  if (St.cfg.shared_layers > 0 && St.cfg.wots_from_tree) {
+    const size_t need = (size_t)St.nkeys * shared_words(set, St.cfg.shared_layers);
+    void* before[2] = {B.shared, B.key_used};
+    CUDA_TRY(h, grow(B.shared, B.shared_cap, need));
+    CUDA_TRY(h, grow(B.key_used, B.key_used_cap, (size_t)St.nkeys));
+    void* after[2] = {B.shared, B.key_used};
+    if (std::memcmp(before, after, sizeof before) != 0) {
+      B.gen++;
+      drop_graphs(h);
+    }
+  }
   St.staged = count;
   return HS_OK;
 }
@@ -467,6 +523,8 @@ void hs_close(hs_t* h) {
     cudaFree(B.plans); cudaFree(B.idx); cudaFree(B.roots); cudaFree(B.froots); cudaFree(B.stash);
     cudaFreeHost(B.h_msgs); cudaFreeHost(B.h_offs); cudaFreeHost(B.h_sigs);
     cudaFree(h->sets[s].keys);
+    cudaFree(B.shared);
+    cudaFree(B.key_used);
     cudaFree(h->sets[s].sk_raw);
   }
   if (h->flush) cudaFree(h->flush);

@@ -19,6 +19,7 @@ enum KernelId : int {
   K_KEYGEN = 6,
   K_VERIFY = 7,
   K_WOTS_GATHER = 8,
+  K_TREE_SHARED = 9,
 };
 
 // variant: 0 = Native, 1 = Imad (sha256.cuh)
@@ -30,5 +31,11 @@ size_t fors_smem_bytes(int trees_per_set, int sets_fused, int relax);
 
 template <int S>
 size_t stash_words_per_msg();
+
+template <int S>
+size_t shared_words_per_key(int layers);
+
+template <int S>
+int shared_max_layers();
 
 }  // namespace hs

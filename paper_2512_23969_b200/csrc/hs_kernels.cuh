@@ -60,6 +60,11 @@ struct LaunchArgs {
   uint32_t* fors_roots;      // count * k * 8 words
   uint8_t* sk_out;           // keygen output (nkeys * 4n)
   uint32_t* stash;           // count * d * wots_len * w * NW words: signing-leaf chains (nullable)
+  // Subtree sharing (top `shared_layers` hypertree layers): per key a table of
+  // every subtree those layers can address, computed once per batch.
+  uint32_t* shared;          // nkeys * units * shared_rec_words(S) (nullable)
+  int shared_layers;         // 0 = off
+  uint8_t* key_used;         // nkeys flags set by msg_prep
   const uint8_t* pks;        // verify: nkeys * 2n (pk_seed || pk_root)
   const uint8_t* vsigs;      // verify: count * sig_bytes
   uint8_t* ok;               // verify: count flags
@@ -170,6 +175,7 @@ __global__ void msg_prep_kernel(LaunchArgs a) {
   pl.leaf = leaf;
   pl.key = key;
   a.plans[i] = pl;
+  if (a.key_used) a.key_used[key] = 1;
   // FORS indices, LSB-first bit order within each byte (sigcore.py:75-90)
   int off = 0;
   for (int g = 0; g < Pr::k; g++) {
@@ -248,7 +254,8 @@ __global__ void __launch_bounds__(kTreeBlock, (S == 2 ? 4 : kTreeMinBlocks)) tre
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
   __shared__ uint32_t tbuf[32 * kTreeBlock];
-  const uint64_t per_msg = (uint64_t)Pr::d * Pr::leaves;
+  // layers >= d - shared_layers come from the shared-subtree table instead
+  const uint64_t per_msg = (uint64_t)(Pr::d - a.shared_layers) * Pr::leaves;
   const uint64_t gid = (uint64_t)blockIdx.x * kTreeBlock + threadIdx.x;
   const bool valid = gid < (uint64_t)a.count * per_msg;
   const uint32_t msg = valid ? (uint32_t)(gid / per_msg) : 0u;
@@ -294,6 +301,85 @@ __global__ void __launch_bounds__(kTreeBlock, (S == 2 ? 4 : kTreeMinBlocks)) tre
     uint32_t* r = a.roots + ((size_t)msg * (Pr::d + 1) + layer + 1) * 8;
 #pragma unroll
     for (int j = 0; j < NW; j++) r[j] = node[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Subtree sharing.  The top layers of the hypertree can only address a few
+// subtrees per key (layer d-1: tree 0; layer d-2: 2^(h/d) trees; ...), so in a
+// batch signed by one key most messages walk the same ones.  A subtree is a
+// pure function of (key, layer, tree) -- identical leaves, nodes and WOTS
+// chains for every message that reaches it -- so TREE_Sign computes each of
+// them once per batch (tree_shared_kernel) and the per-message kernels skip
+// those layers; wots_gather_kernel then reads the message's auth path, root
+// and WOTS chain nodes from the shared record.  Output bytes are unchanged.
+//
+// Record of one shared subtree: nodes of every level ([level][index], 8 words
+// each, levels 0..hp), then all leaves' chains ([leaf][chain][pos][NW]).
+// ---------------------------------------------------------------------------
+template <int S>
+struct Shared {
+  using Pr = P<S>;
+  static constexpr int max_layers = Pr::hp >= 4 ? 2 : 3;
+  static constexpr int node_words = (2 * Pr::leaves - 1) * 8;
+  static constexpr int leaf_stash_words = Pr::wots_len * Pr::w * Pr::NW;
+  static constexpr int rec_words = node_words + Pr::leaves * leaf_stash_words;
+  // units per key for L shared layers: sum_{j<L} 2^(hp*j)
+  __host__ __device__ static constexpr int units(int L) { return L <= 0 ? 0 : units(L - 1) + (1 << (Pr::hp * (L - 1))); }
+  // level offset (in nodes) inside a record
+  __device__ static constexpr int level_off(int lvl) { return lvl == 0 ? 0 : level_off(lvl - 1) + (Pr::leaves >> (lvl - 1)); }
+  // record of (key, layer, tree); layer >= d - L
+  __device__ static uint32_t* rec(const LaunchArgs& a, uint32_t key, int layer, uint64_t tree) {
+    const int j = Pr::d - 1 - layer;  // depth from the top
+    const size_t unit = (size_t)units(j) + (size_t)tree;
+    return a.shared + ((size_t)key * units(a.shared_layers) + unit) * rec_words;
+  }
+};
+
+template <int S, class V>
+__global__ void __launch_bounds__(kTreeBlock, (S == 2 ? 4 : kTreeMinBlocks)) tree_shared_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  using Sh = Shared<S>;
+  constexpr int NW = Pr::NW;
+  __shared__ uint32_t tbuf[32 * kTreeBlock];
+  const int U = Sh::units(a.shared_layers);
+  const uint64_t per_key = (uint64_t)U * Pr::leaves;
+  const uint64_t gid = (uint64_t)blockIdx.x * kTreeBlock + threadIdx.x;
+  const uint32_t key = (uint32_t)(gid / per_key);
+  const bool valid = key < a.nkeys && a.key_used[key];
+  const uint32_t rem = (uint32_t)(gid % per_key);
+  const uint32_t unit = rem / Pr::leaves;
+  const uint32_t leaf = rem % Pr::leaves;
+  int j = 0;
+  while (j + 1 < a.shared_layers && (uint32_t)Sh::units(j + 1) <= unit) j++;
+  const uint32_t layer = Pr::d - 1 - j;
+  const uint64_t tree = unit - Sh::units(j);
+  uint32_t node[8];
+  uint32_t* R = nullptr;
+  const KeyDev& K = a.keys[valid ? key : 0u];
+  if (valid) {
+    R = Sh::rec(a, key, (int)layer, tree);
+    wots_leaf<S, V>(K, layer, tree, leaf, &tbuf[threadIdx.x], kTreeBlock, node,
+                    R + Sh::node_words + (size_t)leaf * Sh::leaf_stash_words);
+#pragma unroll
+    for (int w = 0; w < NW; w++) R[leaf * 8 + w] = node[w];
+  }
+#pragma unroll 1
+  for (int lvl = 1; lvl <= Pr::hp; lvl++) {
+    uint32_t other[NW];
+#pragma unroll
+    for (int w = 0; w < NW; w++) other[w] = __shfl_down_sync(0xffffffffu, node[w], 1u << (lvl - 1));
+    if (valid && (leaf & ((1u << lvl) - 1u)) == 0u) {
+      uint32_t m[2 * NW], mid[8];
+#pragma unroll
+      for (int w = 0; w < NW; w++) { m[w] = node[w]; m[NW + w] = other[w]; }
+#pragma unroll
+      for (int w = 0; w < 8; w++) mid[w] = K.thash_mid[w];
+      thash_reg<V, 2 * NW>(node, mid, make_adrs(layer, tree, ADDR_HASHTREE, 0, (uint32_t)lvl, leaf >> lvl), m);
+      uint32_t* dst = R + (size_t)(Sh::level_off(lvl) + (leaf >> lvl)) * 8;
+#pragma unroll
+      for (int w = 0; w < NW; w++) dst[w] = node[w];
+    }
   }
 }
 
@@ -547,17 +633,45 @@ __global__ void __launch_bounds__(kSmallBlock) wots_gather_kernel(LaunchArgs a) 
   const uint32_t rem = (uint32_t)(gid % per_msg);
   const int layer = (int)(rem / Pr::wots_len);
   const int chain = (int)(rem % Pr::wots_len);
+  using Sh = Shared<S>;
+  const int first_shared = Pr::d - a.shared_layers;
+  const MsgPlan pl = a.plans[msg];
+  uint64_t tree;
+  uint32_t leaf;
+  layer_coords<S>(pl, layer, tree, leaf);
+  // the value this layer signs: the FORS pk, or the root of the layer below
+  const uint32_t* r;
+  if (layer > first_shared) {
+    uint64_t tb;
+    uint32_t lb;
+    layer_coords<S>(pl, layer - 1, tb, lb);
+    r = Sh::rec(a, pl.key, layer - 1, tb) + (size_t)Sh::level_off(Pr::hp) * 8;
+  } else {
+    r = a.roots + ((size_t)msg * (Pr::d + 1) + layer) * 8;
+  }
   uint32_t mw[8];
-  const uint32_t* r = a.roots + ((size_t)msg * (Pr::d + 1) + layer) * 8;
 #pragma unroll
   for (int j = 0; j < NW; j++) mw[j] = r[j];
   const uint32_t digit = wots_digit<S>(mw, chain);
-  const uint32_t* src = a.stash + ((((size_t)msg * Pr::d + layer) * Pr::wots_len + chain) * Pr::w + digit) * NW;
+  uint8_t* lsig = a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_ht + (size_t)layer * Pr::layer_bytes;
+  const uint32_t* src;
+  if (layer >= first_shared) {
+    const uint32_t* R = Sh::rec(a, pl.key, layer, tree);
+    src = R + Sh::node_words + (size_t)leaf * Sh::leaf_stash_words + ((size_t)chain * Pr::w + digit) * NW;
+    if (chain < Pr::hp) {  // auth node of level `chain` (vexec.py:529-532)
+      const uint32_t* sib = R + (size_t)(Sh::level_off(chain) + ((leaf >> chain) ^ 1u)) * 8;
+      uint32_t y[NW];
+#pragma unroll
+      for (int j = 0; j < NW; j++) y[j] = sib[j];
+      store_node<NW>(lsig + Pr::wots_sig_bytes + chain * Pr::n, y);
+    }
+  } else {
+    src = a.stash + ((((size_t)msg * Pr::d + layer) * Pr::wots_len + chain) * Pr::w + digit) * NW;
+  }
   uint32_t x[NW];
 #pragma unroll
   for (int j = 0; j < NW; j++) x[j] = src[j];
-  store_node<NW>(a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_ht + (size_t)layer * Pr::layer_bytes + chain * Pr::n,
-                 x);
+  store_node<NW>(lsig + chain * Pr::n, x);
 }
 
 // ---------------------------------------------------------------------------

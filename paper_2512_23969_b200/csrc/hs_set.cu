@@ -43,7 +43,14 @@ cudaError_t launch_v(int which, const LaunchArgs& a, cudaStream_t s) {
       fors_pk_kernel<S, Native><<<blocks(a.count, kSmallBlock), kSmallBlock, 0, s>>>(a);
       break;
     case K_TREE:
-      tree_sign_kernel<S, V><<<blocks((uint64_t)a.count * Pr::d * Pr::leaves, kTreeBlock), kTreeBlock, 0, s>>>(a);
+      tree_sign_kernel<S, V><<<blocks((uint64_t)a.count * (Pr::d - a.shared_layers) * Pr::leaves, kTreeBlock),
+                               kTreeBlock, 0, s>>>(a);
+      break;
+    case K_TREE_SHARED:
+      if (a.shared_layers <= 0 || a.nkeys == 0) return cudaSuccess;
+      tree_shared_kernel<S, V><<<blocks((uint64_t)a.nkeys * Shared<S>::units(a.shared_layers) * Pr::leaves,
+                                        kTreeBlock),
+                                 kTreeBlock, 0, s>>>(a);
       break;
     case K_WOTS:
       wots_sign_kernel<S, V><<<blocks((uint64_t)a.count * Pr::d * Pr::wots_len, kSmallBlock), kSmallBlock, 0, s>>>(a);
@@ -70,6 +77,16 @@ cudaError_t launch_kernel<HS_SET>(int which, int variant, const LaunchArgs& a, c
   // message preparation, key setup, T_k and verification are a vanishing
   // share of the work: launch_v instantiates them with the native path only
   return variant ? launch_v<HS_SET, Fast>(which, a, s) : launch_v<HS_SET, Native>(which, a, s);
+}
+
+template <>
+size_t shared_words_per_key<HS_SET>(int layers) {
+  return (size_t)Shared<HS_SET>::units(layers) * Shared<HS_SET>::rec_words;
+}
+
+template <>
+int shared_max_layers<HS_SET>() {
+  return Shared<HS_SET>::max_layers;
 }
 
 template <>

@@ -161,15 +161,16 @@ using Fast = Mix<0, 0, 0, true, 1, true, false>;
 // (padding, lengths, zeros, chain-invariant ADRS words) fold.
 template <class V, int R0, int R1>
 __device__ __forceinline__ void sha_rounds(uint32_t s[8], uint32_t* W) {
+  const V v{};  // paths may carry per-call state (e.g. an opaque register)
   uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5], g = s[6], h = s[7];
 #pragma unroll
   for (int i = R0; i < R1; i++) {
     if (i >= 16) {
-      W[i & 15] = V::wnew(V::s1(W[(i - 2) & 15]), W[(i - 7) & 15], V::s0(W[(i - 15) & 15]), W[i & 15]);
+      W[i & 15] = v.wnew(v.s1(W[(i - 2) & 15]), W[(i - 7) & 15], v.s0(W[(i - 15) & 15]), W[i & 15]);
     }
-    const uint32_t t = V::t1(h, Kc(i), W[i & 15], V::S1(e), ch(e, f, g));
-    const uint32_t an = V::anew(t, V::S0(a), maj(a, b, c));
-    h = g; g = f; f = e; e = V::enew(d, t);
+    const uint32_t t = v.t1(h, Kc(i), W[i & 15], v.S1(e), ch(e, f, g));
+    const uint32_t an = v.anew(t, v.S0(a), maj(a, b, c));
+    h = g; g = f; f = e; e = v.enew(d, t);
     d = c; c = b; b = a; a = an;
   }
   s[0] = a; s[1] = b; s[2] = c; s[3] = d; s[4] = e; s[5] = f; s[6] = g; s[7] = h;
@@ -182,8 +183,9 @@ __device__ __forceinline__ void compress(uint32_t st[8], uint32_t W[16]) {
 #pragma unroll
   for (int i = 0; i < 8; i++) s[i] = st[i];
   sha_rounds<V, 0, 64>(s, W);
+  const V v{};
 #pragma unroll
-  for (int i = 0; i < 8; i++) st[i] = V::ff(st[i], s[i]);
+  for (int i = 0; i < 8; i++) st[i] = v.ff(st[i], s[i]);
 }
 
 // Rounds [0, R) only (no schedule expansion needed while R <= 16).
@@ -205,8 +207,9 @@ __device__ __forceinline__ void compress_resume(uint32_t st[8], const uint32_t s
 #pragma unroll
   for (int i = 0; i < 8; i++) s[i] = sR[i];
   sha_rounds<V, R0, 64>(s, W);
+  const V v{};
 #pragma unroll
-  for (int i = 0; i < 8; i++) st[i] = V::ff(st[i], s[i]);
+  for (int i = 0; i < 8; i++) st[i] = v.ff(st[i], s[i]);
 }
 
 // ---------------------------------------------------------------------------

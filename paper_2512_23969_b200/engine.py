@@ -90,6 +90,7 @@ class Engine:
             "chunk": c.chunk,
             "wots_from_tree": bool(c.wots_from_tree),
             "streams": c.streams,
+            "shared_layers": c.shared_layers,
         }
 
     def set_config(self, set_id: str, **kw) -> dict:
@@ -107,6 +108,7 @@ class Engine:
         c.chunk = int(cur["chunk"])
         c.wots_from_tree = int(bool(cur["wots_from_tree"]))
         c.streams = int(cur["streams"])
+        c.shared_layers = int(cur["shared_layers"])
         self._check(_lib.lib().hs_config_set(self._h, SET_INDEX[set_id], ctypes.byref(c)), "hs_config_set")
         return self.config(set_id)
 

@@ -171,3 +171,62 @@ def test_config2_full_batch_128f(eng, config2, streams):
         eng.set_config("128f", **base)
     assert sigs == ref
     assert all(eng.verify_batch("128f", sk[32:], msgs, sigs))
+
+
+def test_graph_signer_stage_plugin(eng, oracle_mod):
+    """The reference's stage-plugin protocol (batchgraph.py:93-131, 245-353) driven by
+    the task-graph scheduler: one GPU batch per instantiated graph set, bytes == oracle."""
+    from paper_2512_23969_b200 import batchgraph as bg
+
+    p = derive("128f")
+    rng = random.Random(11)
+    sk_raw = oracle_mod.keygen("128f", rng.randbytes(48))
+    sk = hs.SecretKey.from_bytes(sk_raw, p)
+    msgs = [rng.randbytes(rng.choice([0, 32, 77])) for _ in range(24)]
+    signer = bg.GraphSigner(sk, p)
+    graphs = bg.build_graphs(msgs, m=8, T=3)
+    pool = bg.BufferPool()
+    sigs, log = bg.execute_graphs(graphs, 4, signer, pool=pool, rng=random.Random(3))
+    assert bg.replay_check(log, graphs)
+    assert signer.launches == 1 and pool.allocations == len(msgs)
+    assert sigs == [oracle_mod.sign("128f", sk_raw, m) for m in msgs]
+
+
+def test_config_apply_roundtrip(eng, tmp_path):
+    from paper_2512_23969_b200.config import TuningConfig
+
+    before = {s: eng.config(s) for s in SETS}
+    cfg = TuningConfig.from_engine(eng)
+    cfg.sets["192f"].b200.update(fors_trees_per_set=2, fors_sets_fused=4, fors_relax=True, streams=3)
+    path = tmp_path / "t.json"
+    cfg.save(path)
+    try:
+        TuningConfig.load(path).apply(eng)
+        c = eng.config("192f")
+        assert (c["fors_trees_per_set"], c["fors_sets_fused"], c["fors_relax"], c["streams"]) == (2, 4, True, 3)
+    finally:
+        for s, c in before.items():
+            eng.set_config(s, **c)
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_subtree_sharing(eng, oracle_mod, set_id):
+    """Shared top-layer subtrees (0 .. max layers) with two keys in one batch: bytes == oracle."""
+    p = derive(set_id)
+    rng = random.Random(21 + p.n)
+    sks = [oracle_mod.keygen(set_id, rng.randbytes(3 * p.n)) for _ in range(2)]
+    count = 96
+    msgs = [rng.randbytes(32) for _ in range(count)]
+    kidx = [rng.randrange(2) for _ in range(count)]
+    ref, _ = oracle_mod.sign_many(set_id, b"".join(sks), kidx, msgs)
+    eng.upload_keys(set_id, sks)
+    base = eng.config(set_id)
+    top = 2 if set_id == "256f" else 3
+    try:
+        for L in range(top + 1):
+            eng.set_config(set_id, shared_layers=L)
+            assert eng.sign_batch(set_id, msgs, key_idx=kidx) == ref, L
+        with pytest.raises(hs.ConfigError):
+            eng.set_config(set_id, shared_layers=top + 1)
+    finally:
+        eng.set_config(set_id, **base)

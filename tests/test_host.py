@@ -102,3 +102,13 @@ def test_message_to_indices_lsb_first(golden):
     for set_id in SETS:
         for v in golden["sets"][set_id]["h_msg"]:
             assert hs.message_to_indices(bytes.fromhex(v["mhash"]), set_id) == v["indices"]
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_subtree_work_matches_reference_counter(golden, set_id):
+    from paper_2512_23969_b200.params import shared_units, subtree_compressions
+
+    assert subtree_compressions(set_id) == golden["sets"][set_id]["tree_layer"]["compressions"]
+    p = derive(set_id)
+    assert shared_units(set_id, 0) == 0 and shared_units(set_id, 1) == 1
+    assert shared_units(set_id, 2) == 1 + p.subtree_leaves
