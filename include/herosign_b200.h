@@ -72,7 +72,11 @@ typedef struct {
   int32_t shared_layers;      /* top hypertree layers whose subtrees are
                                  computed once per (key, tree) per batch
                                  instead of once per message (0 = off; max
-                                 3 for 128f/192f, 2 for 256f)                */
+                                 4 for 128f/192f, 3 for 256f)                */
+  int32_t shared_auto;        /* 1: per batch, share a layer only when its
+                                 shareable subtrees are fewer than half the
+                                 messages (and within the table budget);
+                                 0: share exactly shared_layers              */
 } hs_set_config;
 
 HS_API int hs_open(int device, hs_t **out);

@@ -46,6 +46,7 @@ class SetConfig(ctypes.Structure):
         ("wots_from_tree", ctypes.c_int32),
         ("streams", ctypes.c_int32),
         ("shared_layers", ctypes.c_int32),
+        ("shared_auto", ctypes.c_int32),
     ]
 
 

@@ -58,7 +58,7 @@ class TuningConfig:
                         "WOTS_Sign": "tuned" if tuned_all else "baseline"}
             b200 = dict(B200_DEFAULTS[set_id])
             b200.update({"variant": {k: 0 for k in KERNELS}, "wots_from_tree": True, "chunk": 16384, "streams": 1,
-                         "shared_layers": 2 if set_id == "256f" else 3})
+                         "shared_layers": 3 if set_id == "256f" else 4, "shared_auto": True})
             sets[set_id] = SetConfig(best, padding_solve(p.n), backends, set_id == "256f", b200)
         return cls(seme_per_block=seme, sets=sets)
 
@@ -96,7 +96,7 @@ class TuningConfig:
             b = dict(cfg.b200) if cfg.b200 else {}
             kw = {}
             for key in ("fors_trees_per_set", "fors_sets_fused", "fors_relax", "wots_from_tree", "chunk", "streams",
-                        "shared_layers"):
+                        "shared_layers", "shared_auto"):
                 if key in b:
                     kw[key] = b[key]
             if "variant" in b:
@@ -114,7 +114,7 @@ class TuningConfig:
                 "fors_trees_per_set": e["fors_trees_per_set"], "fors_sets_fused": e["fors_sets_fused"],
                 "fors_relax": e["fors_relax"], "variant": {k: e["variant"][k] for k in KERNELS},
                 "wots_from_tree": e["wots_from_tree"], "chunk": e["chunk"], "streams": e["streams"],
-                "shared_layers": e["shared_layers"],
+                "shared_layers": e["shared_layers"], "shared_auto": e["shared_auto"],
             }
             cfg.sets[set_id].backends = {k: "tuned" if e["variant"][k] else "baseline" for k in KERNELS}
         return cfg

@@ -99,8 +99,9 @@ hs_set_config default_config(int set) {
   c.use_graph = 1;
   c.chunk = 16384;
   c.wots_from_tree = 1;
-  c.streams = 1;
+  c.streams = 2;
   c.shared_layers = shared_max(set);
+  c.shared_auto = 1;
   return c;
 }
 
@@ -156,11 +157,13 @@ struct SetState {
   // staged batch
   uint32_t staged = 0;
   bool has_keyidx = false, has_optrand = false;
+  int shared_eff = 0;  // subtree-sharing depth chosen for the staged batch
 };
 
 using GraphKey = std::tuple<int, uint32_t, int, int, uint64_t, std::string>;
 
 constexpr int kMaxStreams = 8;
+constexpr size_t kSharedBudgetBytes = (size_t)8 << 30;  // shared-subtree table cap
 
 }  // namespace
 
@@ -181,8 +184,11 @@ struct hs_ctx {
   int sm_count = 0, smem_optin = 0, cc_major = 0, cc_minor = 0;
   void* flush = nullptr;
   size_t flush_cap = 0;
-  cudaStream_t ls[kMaxStreams] = {};   // sub-batch launch streams
+  cudaStream_t ls[kMaxStreams] = {};   // D2H copy streams
+  cudaStream_t q[kMaxStreams] = {};    // sub-batch compute streams, descending priority
   cudaEvent_t staged = nullptr, ls_done[kMaxStreams] = {};
+  cudaEvent_t done[kMaxStreams] = {}, joins[kMaxStreams] = {}, sh_done = nullptr;
+  int last_T = 1;
 };
 
 namespace {
@@ -208,8 +214,8 @@ bool valid_set(int set) { return set >= 0 && set <= 2; }
 
 std::string cfg_fingerprint(const hs_set_config& c) {
   char b[160];
-  snprintf(b, sizeof b, "%d/%d/%d/%d%d%d%d/%d/%d", c.fors_trees_per_set, c.fors_sets_fused, c.fors_relax,
-           c.variant[0], c.variant[1], c.variant[2], c.variant[3], c.wots_from_tree, c.shared_layers);
+  snprintf(b, sizeof b, "%d/%d/%d/%d%d%d%d/%d/%d/%d", c.fors_trees_per_set, c.fors_sets_fused, c.fors_relax,
+           c.variant[0], c.variant[1], c.variant[2], c.variant[3], c.wots_from_tree, c.shared_layers, c.shared_auto);
   return b;
 }
 
@@ -238,6 +244,7 @@ int check_layout(hs_t* h, int set, const hs_set_config& c) {
   if (c.streams < 1 || c.streams > kMaxStreams) return fail(h, HS_E_CONFIG, "streams must be in 1..%d", kMaxStreams);
   if (c.shared_layers < 0 || c.shared_layers > shared_max(set))
     return fail(h, HS_E_CONFIG, "shared_layers must be in 0..%d for this set", shared_max(set));
+  if (c.shared_auto != 0 && c.shared_auto != 1) return fail(h, HS_E_CONFIG, "shared_auto must be 0 or 1");
   return HS_OK;
 }
 
@@ -292,7 +299,7 @@ LaunchArgs make_args(hs_t* h, int set, uint32_t first, uint32_t count) {
                 ? B.stash + (size_t)first * sw
                 : nullptr;
   // subtree sharing needs the stash (WOTS gather) and a table sized for the key set
-  const int L = St.cfg.shared_layers;
+  const int L = St.shared_eff;
   if (a.stash && L > 0 && B.shared && B.shared_cap >= (size_t)St.nkeys * shared_words(set, L) && B.key_used &&
       B.key_used_cap >= St.nkeys) {
     a.shared = B.shared;
@@ -350,74 +357,116 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
   return cudaSuccess;
 }
 
-// One sub-batch as a CUDA graph (captured once per shape and offset) or as
-// plain stream launches.  The graph is launched on `launch_stream`.
-int run_one(hs_t* h, int set, uint32_t first, uint32_t count, int mode, cudaStream_t launch_stream) {
-  SetState& St = h->sets[set];
-  const LaunchArgs a = make_args(h, set, first, count);
-  const bool serial = mode == 1;
-  if (!serial && St.cfg.use_graph) {
-    GraphKey key{set, count, St.has_keyidx ? 1 : 0, St.has_optrand ? 1 : 0, h->buf[set].gen,
-                 cfg_fingerprint(St.cfg) + "/" + std::to_string((uintptr_t)St.keys) + "/" + std::to_string(St.nkeys) +
-                     "/" + std::to_string(first)};
-    auto it = h->graphs.find(key);
-    if (it == h->graphs.end()) {
-      cudaGraph_t g;
-      CUDA_TRY(h, cudaStreamBeginCapture(h->s0, cudaStreamCaptureModeThreadLocal));
-      cudaError_t e = enqueue(h, set, a, true, false);
-      cudaError_t e2 = cudaStreamEndCapture(h->s0, &g);
-      if (e != cudaSuccess) return fail(h, HS_E_CUDA, "capture: %s", cudaGetErrorString(e));
-      if (e2 != cudaSuccess) return fail(h, HS_E_CUDA, "end capture: %s", cudaGetErrorString(e2));
-      cudaGraphExec_t ex;
-      CUDA_TRY(h, cudaGraphInstantiate(&ex, g, 0));
-      cudaGraphDestroy(g);
-      h->launches -= h->last_kernels;  // capture does not launch
-      h->graph_kernels[key] = h->last_kernels;
-      it = h->graphs.emplace(key, ex).first;
-    }
-    CUDA_TRY(h, cudaGraphLaunch(it->second, launch_stream));
-    h->launches += h->graph_kernels[key];
-  } else {
-    CUDA_TRY(h, enqueue(h, set, a, false, serial));
+// Multi-stream batch (the paper's m x T batching), one
+// graph per batch shape:
+//
+//   s0: [memset key_used] -> msg_prep(all) -> fork
+//   q0: [shared subtrees] ...................................-> sh
+//   qj: FORS_j -> T_k_j -> TREE_j -> (wait sh) -> WOTS_j -> done_j -> join
+//
+// Sub-batch j's stream qj has the j-th highest priority and the graph is
+// instantiated with per-node priorities, so the block scheduler drains
+// sub-batch 0 first while later ones fill the idle slots and the tail; each
+// sub-batch's signatures are complete (event done_j) while the others still
+// run, so their D2H copies (issued on ls[j] outside the graph) overlap the
+// remaining compute.  The shared-subtree kernel runs once for the whole batch.
+cudaError_t enqueue_batch(hs_t* h, int set, uint32_t count, int T, bool capture) {
+  const hs_set_config& c = h->sets[set].cfg;
+  const LaunchArgs all = make_args(h, set, 0, count);
+  auto rec = [&](cudaEvent_t ev, cudaStream_t s) {
+    return capture ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal) : cudaEventRecord(ev, s);
+  };
+  cudaError_t e;
+  int kernels = 0;
+#define TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
+  TRY(rec(h->ev[0], h->s0));
+  if (all.shared_layers > 0) TRY(cudaMemsetAsync(all.key_used, 0, all.nkeys, h->s0));
+  TRY(launch(set, K_PREP, c.variant[3], all, h->s0));
+  kernels++;
+  TRY(rec(h->ev[1], h->s0));
+  TRY(cudaEventRecord(h->fork, h->s0));
+  if (all.shared_layers > 0) {
+    TRY(cudaStreamWaitEvent(h->q[0], h->fork, 0));
+    TRY(launch(set, K_TREE_SHARED, c.variant[1], all, h->q[0]));
+    TRY(cudaEventRecord(h->sh_done, h->q[0]));
+    kernels++;
   }
-  return HS_OK;
-}
-
-// Sub-batch split: T = cfg.streams graphs on T launch streams run
-// concurrently (the paper's m x T multi-stream batching),
-// so one graph's FORS/TREE tail overlaps the others' bulk.  `fetch_to`
-// (optional, pinned host memory) receives each sub-batch's signatures from
-// its own stream as soon as it is done, overlapping D2H with compute.
-int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nullptr) {
-  if (count == 0) return HS_OK;
-  h->last_set = set;
-  h->last_mode = mode;
-  const size_t sb = (size_t)kInfo[set].sig_bytes;
-  int T = std::max(1, std::min(h->sets[set].cfg.streams, kMaxStreams));
-  // sub-batches would race on the per-batch shared-subtree table
-  if (mode == 1 || !h->sets[set].cfg.use_graph || h->sets[set].cfg.shared_layers > 0) T = 1;
-  T = (int)std::min<uint32_t>((uint32_t)T, std::max<uint32_t>(1u, count / 64u));
-  if (T == 1) {
-    int rc = run_one(h, set, 0, count, mode, h->s0);
-    if (rc) return rc;
-    if (fetch_to)
-      CUDA_TRY(h, cudaMemcpyAsync(fetch_to, h->buf[set].sigs, count * sb, cudaMemcpyDeviceToHost, h->s0));
-    return HS_OK;
-  }
-  CUDA_TRY(h, cudaEventRecord(h->staged, h->s0));
   const uint32_t per = (count + T - 1) / T;
   for (int j = 0; j < T; j++) {
     const uint32_t first = (uint32_t)j * per;
     if (first >= count) break;
     const uint32_t cn = std::min(per, count - first);
-    CUDA_TRY(h, cudaStreamWaitEvent(h->ls[j], h->staged, 0));
-    int rc = run_one(h, set, first, cn, mode, h->ls[j]);
-    if (rc) return rc;
+    const LaunchArgs a = make_args(h, set, first, cn);
+    cudaStream_t q = h->q[j];
+    TRY(cudaStreamWaitEvent(q, h->fork, 0));
+    TRY(launch(set, K_FORS, c.variant[0], a, q));
+    TRY(launch(set, K_FORSPK, c.variant[0], a, q));
+    TRY(launch(set, K_TREE, c.variant[1], a, q));
+    if (all.shared_layers > 0) TRY(cudaStreamWaitEvent(q, h->sh_done, 0));
+    TRY(launch(set, a.stash ? K_WOTS_GATHER : K_WOTS, c.variant[2], a, q));
+    kernels += 4;
+    TRY(rec(h->done[j], q));
+    TRY(cudaEventRecord(h->joins[j], q));
+    TRY(cudaStreamWaitEvent(h->s0, h->joins[j], 0));
+  }
+  TRY(rec(h->ev[4], h->s0));
+#undef TRY
+  h->launches += kernels;
+  h->last_kernels = kernels;
+  return cudaSuccess;
+}
+
+int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nullptr) {
+  if (count == 0) return HS_OK;
+  SetState& St = h->sets[set];
+  h->last_set = set;
+  h->last_mode = mode;
+  const size_t sb = (size_t)kInfo[set].sig_bytes;
+  if (mode == 1) {  // serialised kernels with per-kernel events (roofline timing)
+    CUDA_TRY(h, enqueue(h, set, make_args(h, set, 0, count), false, true));
     if (fetch_to)
+      CUDA_TRY(h, cudaMemcpyAsync(fetch_to, h->buf[set].sigs, count * sb, cudaMemcpyDeviceToHost, h->s0));
+    return HS_OK;
+  }
+  int T = std::max(1, std::min(St.cfg.streams, kMaxStreams));
+  T = (int)std::min<uint32_t>((uint32_t)T, std::max<uint32_t>(1u, count / 256u));
+  h->last_T = T;
+  if (St.cfg.use_graph) {
+    GraphKey key{set, count, St.has_keyidx ? 1 : 0, St.has_optrand ? 1 : 0, h->buf[set].gen,
+                 cfg_fingerprint(St.cfg) + "/" + std::to_string((uintptr_t)St.keys) + "/" + std::to_string(St.nkeys) +
+                     "/L" + std::to_string(St.shared_eff) + "/T" + std::to_string(T)};
+    auto it = h->graphs.find(key);
+    if (it == h->graphs.end()) {
+      cudaGraph_t g;
+      CUDA_TRY(h, cudaStreamBeginCapture(h->s0, cudaStreamCaptureModeThreadLocal));
+      cudaError_t e = enqueue_batch(h, set, count, T, true);
+      cudaError_t e2 = cudaStreamEndCapture(h->s0, &g);
+      if (e != cudaSuccess) return fail(h, HS_E_CUDA, "capture: %s", cudaGetErrorString(e));
+      if (e2 != cudaSuccess) return fail(h, HS_E_CUDA, "end capture: %s", cudaGetErrorString(e2));
+      cudaGraphExec_t ex;
+      CUDA_TRY(h, cudaGraphInstantiateWithFlags(&ex, g, cudaGraphInstantiateFlagUseNodePriority));
+      cudaGraphDestroy(g);
+      h->launches -= h->last_kernels;  // capture does not launch
+      h->graph_kernels[key] = h->last_kernels;
+      it = h->graphs.emplace(key, ex).first;
+    }
+    CUDA_TRY(h, cudaGraphLaunch(it->second, h->s0));
+    h->launches += h->graph_kernels[key];
+  } else {
+    CUDA_TRY(h, enqueue_batch(h, set, count, T, false));
+  }
+  if (fetch_to) {
+    const uint32_t per = (count + T - 1) / T;
+    for (int j = 0; j < T; j++) {
+      const uint32_t first = (uint32_t)j * per;
+      if (first >= count) break;
+      const uint32_t cn = std::min(per, count - first);
+      CUDA_TRY(h, cudaStreamWaitEvent(h->ls[j], h->done[j], 0));
       CUDA_TRY(h, cudaMemcpyAsync(fetch_to + first * sb, h->buf[set].sigs + first * sb, cn * sb,
                                   cudaMemcpyDeviceToHost, h->ls[j]));
-    CUDA_TRY(h, cudaEventRecord(h->ls_done[j], h->ls[j]));
-    CUDA_TRY(h, cudaStreamWaitEvent(h->s0, h->ls_done[j], 0));
+      CUDA_TRY(h, cudaEventRecord(h->ls_done[j], h->ls[j]));
+      CUDA_TRY(h, cudaStreamWaitEvent(h->s0, h->ls_done[j], 0));
+    }
   }
   return HS_OK;
 }
@@ -449,8 +498,30 @@ int stage_inputs(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, co
   if (opt_rand)
     CUDA_TRY(h, cudaMemcpyAsync(B.optrand, opt_rand + (size_t)first * I.n, (size_t)count * I.n,
                                 cudaMemcpyHostToDevice, h->s0));
+  // Subtree sharing depth for this batch: at most cfg.shared_layers, within
+  // the table budget, and (auto policy) only layers whose shareable subtrees
+  // are clearly fewer than the messages that would otherwise recompute them.
+  St.shared_eff = 0;
   if (St.cfg.shared_layers > 0 && St.cfg.wots_from_tree) {
-    const size_t need = (size_t)St.nkeys * shared_words(set, St.cfg.shared_layers);
+    uint32_t used = 1;
+    if (key_idx) {
+      std::vector<uint8_t> seen(St.nkeys, 0);
+      used = 0;
+      for (uint32_t i = 0; i < count; i++)
+        if (!seen[key_idx[first + i]]) { seen[key_idx[first + i]] = 1; used++; }
+    }
+    const int hp = kInfo[set].hp;
+    int L = 0;
+    while (L < St.cfg.shared_layers) {
+      const size_t units_j = (size_t)1 << (hp * L);  // subtrees at depth L per key
+      if (St.cfg.shared_auto && units_j * used * 2 > count) break;
+      if ((size_t)St.nkeys * shared_words(set, L + 1) * 4 > kSharedBudgetBytes) break;
+      L++;
+    }
+    St.shared_eff = L;
+  }
+  if (St.shared_eff > 0) {
+    const size_t need = (size_t)St.nkeys * shared_words(set, St.shared_eff);
     void* before[2] = {B.shared, B.key_used};
     CUDA_TRY(h, grow(B.shared, B.shared_cap, need));
     CUDA_TRY(h, grow(B.key_used, B.key_used_cap, (size_t)St.nkeys));
@@ -500,10 +571,16 @@ int hs_open(int device, hs_t** out) {
     return HS_E_CUDA;
   }
   for (auto& ev : h->ev) cudaEventCreate(&ev);
+  int prio_least = 0, prio_greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest);
   for (int j = 0; j < kMaxStreams; j++) {
     cudaStreamCreateWithFlags(&h->ls[j], cudaStreamNonBlocking);
+    cudaStreamCreateWithPriority(&h->q[j], cudaStreamNonBlocking, std::min(prio_greatest + j, prio_least));
     cudaEventCreateWithFlags(&h->ls_done[j], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&h->done[j], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&h->joins[j], cudaEventDisableTiming);
   }
+  cudaEventCreateWithFlags(&h->sh_done, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->staged, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->join, cudaEventDisableTiming);
@@ -530,8 +607,12 @@ void hs_close(hs_t* h) {
   if (h->flush) cudaFree(h->flush);
   for (int j = 0; j < kMaxStreams; j++) {
     cudaStreamDestroy(h->ls[j]);
+    cudaStreamDestroy(h->q[j]);
     cudaEventDestroy(h->ls_done[j]);
+    cudaEventDestroy(h->done[j]);
+    cudaEventDestroy(h->joins[j]);
   }
+  cudaEventDestroy(h->sh_done);
   cudaEventDestroy(h->staged);
   for (auto& ev : h->ev) cudaEventDestroy(ev);
   cudaEventDestroy(h->fork);
@@ -761,10 +842,13 @@ int hs_timings(hs_t* h, float* ms, int cap) {
   float v[5] = {0, 0, 0, 0, 0};
   cudaEventElapsedTime(&v[0], h->ev[0], h->ev[4]);
   cudaEventElapsedTime(&v[1], h->ev[0], h->ev[1]);
-  cudaEventElapsedTime(&v[2], h->ev[1], h->ev[2]);
-  if (h->last_mode == 1) cudaEventElapsedTime(&v[3], h->ev[2], h->ev[3]);
-  else cudaEventElapsedTime(&v[3], h->ev[1], h->ev[3]);
-  cudaEventElapsedTime(&v[4], h->ev[5], h->ev[4]);
+  if (h->last_mode == 1) cudaEventElapsedTime(&v[2], h->ev[1], h->ev[2]);
+  if (h->last_mode == 1) {
+    cudaEventElapsedTime(&v[3], h->ev[2], h->ev[3]);
+    cudaEventElapsedTime(&v[4], h->ev[5], h->ev[4]);
+  } else {
+    v[2] = v[3] = v[4] = 0.f;  // graph mode overlaps the stages; per-kernel times need mode 1
+  }
   int m = std::min(cap, 5);
   for (int i = 0; i < m; i++) ms[i] = v[i];
   return m;

@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kTreeBlock, (S == 2 ? 4 : kTreeMinBlocks)) tre
 template <int S>
 struct Shared {
   using Pr = P<S>;
-  static constexpr int max_layers = Pr::hp >= 4 ? 2 : 3;
+  static constexpr int max_layers = Pr::hp >= 4 ? 3 : 4;
   static constexpr int node_words = (2 * Pr::leaves - 1) * 8;
   static constexpr int leaf_stash_words = Pr::wots_len * Pr::w * Pr::NW;
   static constexpr int rec_words = node_words + Pr::leaves * leaf_stash_words;

@@ -91,6 +91,7 @@ class Engine:
             "wots_from_tree": bool(c.wots_from_tree),
             "streams": c.streams,
             "shared_layers": c.shared_layers,
+            "shared_auto": bool(c.shared_auto),
         }
 
     def set_config(self, set_id: str, **kw) -> dict:
@@ -109,6 +110,7 @@ class Engine:
         c.wots_from_tree = int(bool(cur["wots_from_tree"]))
         c.streams = int(cur["streams"])
         c.shared_layers = int(cur["shared_layers"])
+        c.shared_auto = int(bool(cur["shared_auto"]))
         self._check(_lib.lib().hs_config_set(self._h, SET_INDEX[set_id], ctypes.byref(c)), "hs_config_set")
         return self.config(set_id)
 

@@ -221,11 +221,13 @@ def test_subtree_sharing(eng, oracle_mod, set_id):
     ref, _ = oracle_mod.sign_many(set_id, b"".join(sks), kidx, msgs)
     eng.upload_keys(set_id, sks)
     base = eng.config(set_id)
-    top = 2 if set_id == "256f" else 3
+    top = 3 if set_id == "256f" else 4
     try:
         for L in range(top + 1):
-            eng.set_config(set_id, shared_layers=L)
+            eng.set_config(set_id, shared_layers=L, shared_auto=False)
             assert eng.sign_batch(set_id, msgs, key_idx=kidx) == ref, L
+        eng.set_config(set_id, shared_layers=top, shared_auto=True)
+        assert eng.sign_batch(set_id, msgs, key_idx=kidx) == ref
         with pytest.raises(hs.ConfigError):
             eng.set_config(set_id, shared_layers=top + 1)
     finally:
