@@ -393,6 +393,7 @@ __global__ void __launch_bounds__(kTreeBlock, (S == 2 ? 4 : kTreeMinBlocks)) tre
 // ---------------------------------------------------------------------------
 // 768 lanes keep the register budget at 85 per thread (65536 / 768).
 constexpr int kForsMaxLanes = 768;
+constexpr int kForsPrefixWords = 16;  // per-message PRF / F prefix states at the head of smem
 
 template <int S>
 __host__ __device__ constexpr int fors_smem_words_per_tree(bool relax) {
@@ -400,14 +401,56 @@ __host__ __device__ constexpr int fors_smem_words_per_tree(bool relax) {
   return relax ? (P<S>::t / 4 + P<S>::t / 2) * P<S>::NW : (P<S>::t + P<S>::t / 2) * P<S>::NW;
 }
 
-// FORS leaf (oracle.py:101-110): sk = PRF(adrs(height 0, index)), leaf = F(sk)
+// FORS leaf (oracle.py:101-110): sk = PRF(adrs(height 0, index)), leaf = F(sk).
+// For a given message every FORS leaf address differs only in the tree index
+// (ADRS bytes 20..21; index < 2^16), so the PRF's first NW+5 message words
+// (SK.seed, ADRS words 0..4) and F's first 5 are fixed per message: those
+// SHA-256 rounds are computed once per CTA (`pre`, shared memory: PRF state
+// after NW+5 rounds, F state after 5) and every leaf resumes from them.
 template <int S, class V>
-__device__ __forceinline__ void fors_leaf(const uint32_t mid[8], const uint32_t* sks, Adrs& fa, uint32_t gidx,
-                                          uint32_t sk_out[8], uint32_t leaf_out[8]) {
+__device__ __forceinline__ void fors_prefix(const uint32_t mid[8], const uint32_t* sks, const Adrs& fa,
+                                            uint32_t* pre) {
   constexpr int NW = P<S>::NW;
-  adrs_set_chain_hash(fa, 0, gidx);
-  prf_reg<V, NW>(sk_out, sks, fa);
-  thash_reg<V, NW>(leaf_out, mid, fa, sk_out);
+  uint32_t W[16], s1[8], s2[8];
+#pragma unroll
+  for (int j = 0; j < NW; j++) W[j] = sks[j];
+  W[NW + 0] = fa.w0; W[NW + 1] = fa.w1; W[NW + 2] = fa.w2; W[NW + 3] = fa.w3; W[NW + 4] = fa.w4;
+#pragma unroll
+  for (int i = 0; i < 8; i++) { s1[i] = IVc(i); s2[i] = mid[i]; }
+  rounds_prefix<V, NW + 5>(s1, W);
+  const uint32_t W2[5] = {fa.w0, fa.w1, fa.w2, fa.w3, fa.w4};
+  rounds_prefix<V, 5>(s2, W2);
+#pragma unroll
+  for (int i = 0; i < 8; i++) { pre[i] = s1[i]; pre[8 + i] = s2[i]; }
+}
+
+template <int S, class V>
+__device__ __forceinline__ void fors_leaf(const uint32_t mid[8], const uint32_t* sks, const Adrs& fa,
+                                          const uint32_t* pre, uint32_t gidx, uint32_t sk_out[8],
+                                          uint32_t leaf_out[8]) {
+  constexpr int NW = P<S>::NW;
+  uint32_t W[16], sR[8];
+#pragma unroll
+  for (int j = 0; j < NW; j++) W[j] = sks[j];
+  W[NW + 0] = fa.w0; W[NW + 1] = fa.w1; W[NW + 2] = fa.w2; W[NW + 3] = fa.w3; W[NW + 4] = fa.w4;
+  W[NW + 5] = (gidx << 16) | 0x8000u;
+#pragma unroll
+  for (int j = NW + 6; j < 15; j++) W[j] = 0;
+  W[15] = (uint32_t)((4 * NW + 22) * 8);
+#pragma unroll
+  for (int i = 0; i < 8; i++) { sk_out[i] = IVc(i); sR[i] = pre[i]; }
+  compress_resume<V, NW + 5>(sk_out, sR, W);
+  W[0] = fa.w0; W[1] = fa.w1; W[2] = fa.w2; W[3] = fa.w3; W[4] = fa.w4;
+  W[5] = join16(gidx, sk_out[0]);
+#pragma unroll
+  for (int j = 1; j < NW; j++) W[5 + j] = join16(sk_out[j - 1], sk_out[j]);
+  W[5 + NW] = (sk_out[NW - 1] << 16) | 0x8000u;
+#pragma unroll
+  for (int j = 6 + NW; j < 15; j++) W[j] = 0;
+  W[15] = (uint32_t)((64 + 22 + 4 * NW) * 8);
+#pragma unroll
+  for (int i = 0; i < 8; i++) { leaf_out[i] = mid[i]; sR[i] = pre[8 + i]; }
+  compress_resume<V, 5>(leaf_out, sR, W);
 }
 
 template <int S, class V>
@@ -433,8 +476,9 @@ __global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) 
   // X[w * S_X + tl * cap_X + j], so a lane's two children are one 8-byte
   // shared load per word and a warp's accesses are bank-conflict free
   const int SA = tpc * capA, SB = tpc * (t / 2);
-  uint32_t* regA = sm;                                 // [NW][tpc][capA]
-  uint32_t* regB = sm + (size_t)NW * SA;               // [NW][tpc][t/2]
+  uint32_t* pre = sm;                                  // [16] per-message SHA-256 prefix states
+  uint32_t* regA = sm + kForsPrefixWords;              // [NW][tpc][capA]
+  uint32_t* regB = regA + (size_t)NW * SA;             // [NW][tpc][t/2]
 
   const MsgPlan pl = a.plans[msg];
   const KeyDev& K = a.keys[pl.key];
@@ -446,10 +490,13 @@ __global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) 
   const uint16_t* idx = a.indices + (size_t)msg * Pr::k;
   uint8_t* fsig = a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_fors;
   constexpr int tree_sig = (1 + Pr::log_t) * Pr::n;    // sk || auth[log_t]
-  Adrs fa = make_adrs(0, pl.tree, ADDR_FORS_TREE, pl.leaf, 0, 0);
+  const Adrs fa = make_adrs(0, pl.tree, ADDR_FORS_TREE, pl.leaf, 0, 0);
+
+  const int tid = threadIdx.x;
+  if (tid == 0) fors_prefix<S, V>(mid, sks, fa, pre);
+  __syncthreads();
 
   // ---- leaf phase (vexec.py:387-435) ----
-  const int tid = threadIdx.x;
   const int tree_in_set = tid / lanes_per_tree;
   const int lane_leaf = tid % lanes_per_tree;
 #pragma unroll 1
@@ -460,7 +507,7 @@ __global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) 
     const uint32_t sel = idx[g];
     if (!relax) {
       uint32_t sk[8], lf[8];
-      fors_leaf<S, V>(mid, sks, fa, (uint32_t)(g * t + lane_leaf), sk, lf);
+      fors_leaf<S, V>(mid, sks, fa, pre, (uint32_t)(g * t + lane_leaf), sk, lf);
       if ((uint32_t)lane_leaf == sel) store_node<NW>(fsig + g * tree_sig, sk);
       uint32_t* dst = regA + (size_t)tl * capA + lane_leaf;
 #pragma unroll
@@ -468,16 +515,17 @@ __global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) 
     } else {
       uint32_t sk0[8], l0[8], sk1[8], l1[8];
       const uint32_t j2 = 2u * lane_leaf;
-      fors_leaf<S, V>(mid, sks, fa, (uint32_t)(g * t) + j2, sk0, l0);
-      fors_leaf<S, V>(mid, sks, fa, (uint32_t)(g * t) + j2 + 1u, sk1, l1);
+      fors_leaf<S, V>(mid, sks, fa, pre, (uint32_t)(g * t) + j2, sk0, l0);
+      fors_leaf<S, V>(mid, sks, fa, pre, (uint32_t)(g * t) + j2 + 1u, sk1, l1);
       if (j2 == sel) store_node<NW>(fsig + g * tree_sig, sk0);
       if (j2 + 1u == sel) store_node<NW>(fsig + g * tree_sig, sk1);
       if ((sel >> 1) == (uint32_t)lane_leaf) store_node<NW>(fsig + g * tree_sig + Pr::n, (sel & 1u) ? l0 : l1);
       uint32_t m[2 * NW], par[8];
 #pragma unroll
       for (int j = 0; j < NW; j++) { m[j] = l0[j]; m[NW + j] = l1[j]; }
-      adrs_set_chain_hash(fa, 1, (uint32_t)lane_leaf + ((uint32_t)(g * t) >> 1));
-      thash_reg<V, 2 * NW>(par, mid, fa, m);
+      Adrs pa = fa;
+      adrs_set_chain_hash(pa, 1, (uint32_t)lane_leaf + ((uint32_t)(g * t) >> 1));
+      thash_reg<V, 2 * NW>(par, mid, pa, m);
       uint32_t* dst = regB + (size_t)tl * (t / 2) + lane_leaf;
 #pragma unroll
       for (int j = 0; j < NW; j++) dst[(size_t)j * SB] = par[j];

@@ -32,7 +32,7 @@ cudaError_t launch_v(int which, const LaunchArgs& a, cudaStream_t s) {
       const int tpc = a.fors_trees_per_set * a.fors_sets_fused;
       const int sets_total = (Pr::k + a.fors_trees_per_set - 1) / a.fors_trees_per_set;
       const int passes = (sets_total + a.fors_sets_fused - 1) / a.fors_sets_fused;
-      const size_t smem = (size_t)tpc * fors_smem_words_per_tree<S>(relax) * 4;
+      const size_t smem = ((size_t)tpc * fors_smem_words_per_tree<S>(relax) + kForsPrefixWords) * 4;
       cudaError_t e = cudaFuncSetAttribute(fors_sign_kernel<S, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
       if (e != cudaSuccess) return e;
@@ -96,7 +96,7 @@ size_t stash_words_per_msg<HS_SET>() {
 
 template <>
 size_t fors_smem_bytes<HS_SET>(int trees_per_set, int sets_fused, int relax) {
-  return (size_t)trees_per_set * sets_fused * fors_smem_words_per_tree<HS_SET>(relax != 0) * 4;
+  return ((size_t)trees_per_set * sets_fused * fors_smem_words_per_tree<HS_SET>(relax != 0) + kForsPrefixWords) * 4;
 }
 
 }  // namespace hs

@@ -68,8 +68,9 @@ def test_work_unit_formula(golden, set_id):
 
 def test_fors_smem_accounting(L):
     # ping-pong regions: 1.5 t nodes per tree (0.75 t with relax)
-    assert hs.Engine.fors_smem_bytes("128f", 11, 3, False) == 33 * 96 * 16
-    assert hs.Engine.fors_smem_bytes("256f", 2, 2, True) == 4 * 384 * 32
+    # + 64 bytes of per-message SHA-256 prefix states
+    assert hs.Engine.fors_smem_bytes("128f", 11, 3, False) == 33 * 96 * 16 + 64
+    assert hs.Engine.fors_smem_bytes("256f", 2, 2, True) == 4 * 384 * 32 + 64
 
 
 def test_no_device_fails_loudly(L):
