@@ -232,3 +232,19 @@ def test_subtree_sharing(eng, oracle_mod, set_id):
             eng.set_config(set_id, shared_layers=top + 1)
     finally:
         eng.set_config(set_id, **base)
+
+
+def test_cli_roundtrip(eng, golden, tmp_path):
+    from paper_2512_23969_b200 import cli
+
+    g = golden["sets"]["192f"]
+    sk, pk, msg, sig = (tmp_path / n for n in ("sk", "pk", "m", "sig"))
+    assert cli.main(["keygen", "192f", "--sk", str(sk), "--pk", str(pk), "--seed", g["keygen"]["seed"]]) == 0
+    assert sk.read_bytes().hex() == g["keygen"]["sk"]
+    msg.write_bytes(bytes(32))
+    assert cli.main(["sign", "192f", "--key", str(sk), "--message", str(msg), "--out", str(sig)]) == 0
+    assert sig.read_bytes() == (GOLDEN_DIR / "sig_192f_zero.bin").read_bytes()
+    assert cli.main(["verify", "192f", "--pk", str(pk), "--message", str(msg), "--sig", str(sig)]) == 0
+    msg.write_bytes(b"\x01" + bytes(31))
+    assert cli.main(["verify", "192f", "--pk", str(pk), "--message", str(msg), "--sig", str(sig)]) == 1
+    assert cli.main(["bench", "128f", "--messages", "256"]) == 0
