@@ -185,9 +185,9 @@ struct hs_ctx {
   void* flush = nullptr;
   size_t flush_cap = 0;
   cudaStream_t ls[kMaxStreams] = {};   // D2H copy streams
-  cudaStream_t q[kMaxStreams] = {};    // sub-batch compute streams, descending priority
+  cudaStream_t q[2 * kMaxStreams + 1] = {};  // compute streams, descending priority
   cudaEvent_t staged = nullptr, ls_done[kMaxStreams] = {};
-  cudaEvent_t done[kMaxStreams] = {}, joins[kMaxStreams] = {}, sh_done = nullptr;
+  cudaEvent_t done[kMaxStreams] = {}, joins[kMaxStreams] = {}, fjoin[kMaxStreams] = {}, sh_done = nullptr;
   int last_T = 1;
 };
 
@@ -397,11 +397,17 @@ cudaError_t enqueue_batch(hs_t* h, int set, uint32_t count, int T, bool capture)
     if (first >= count) break;
     const uint32_t cn = std::min(per, count - first);
     const LaunchArgs a = make_args(h, set, first, cn);
-    cudaStream_t q = h->q[j];
+    // TREE_j on priority 1+2j, FORS_j just below it: FORS_j's short CTAs fill
+    // the SMs TREE_j drains before TREE_{j+1} claims them, and the last
+    // sub-batch's FORS fills the final tail.
+    cudaStream_t q = h->q[1 + 2 * j], qf = h->q[2 + 2 * j];
     TRY(cudaStreamWaitEvent(q, h->fork, 0));
-    TRY(launch(set, K_FORS, c.variant[0], a, q));
-    TRY(launch(set, K_FORSPK, c.variant[0], a, q));
+    TRY(cudaStreamWaitEvent(qf, h->fork, 0));
     TRY(launch(set, K_TREE, c.variant[1], a, q));
+    TRY(launch(set, K_FORS, c.variant[0], a, qf));
+    TRY(launch(set, K_FORSPK, c.variant[0], a, qf));
+    TRY(cudaEventRecord(h->fjoin[j], qf));
+    TRY(cudaStreamWaitEvent(q, h->fjoin[j], 0));
     if (all.shared_layers > 0) TRY(cudaStreamWaitEvent(q, h->sh_done, 0));
     TRY(launch(set, a.stash ? K_WOTS_GATHER : K_WOTS, c.variant[2], a, q));
     kernels += 4;
@@ -575,12 +581,14 @@ int hs_open(int device, hs_t** out) {
   cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest);
   for (int j = 0; j < kMaxStreams; j++) {
     cudaStreamCreateWithFlags(&h->ls[j], cudaStreamNonBlocking);
-    cudaStreamCreateWithPriority(&h->q[j], cudaStreamNonBlocking, std::min(prio_greatest + j, prio_least));
+    cudaEventCreateWithFlags(&h->fjoin[j], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->ls_done[j], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->done[j], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->joins[j], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&h->sh_done, cudaEventDisableTiming);
+  for (int j = 0; j < 2 * kMaxStreams + 1; j++)
+    cudaStreamCreateWithPriority(&h->q[j], cudaStreamNonBlocking, std::min(prio_greatest + j, prio_least));
   cudaEventCreateWithFlags(&h->staged, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->join, cudaEventDisableTiming);
@@ -607,12 +615,13 @@ void hs_close(hs_t* h) {
   if (h->flush) cudaFree(h->flush);
   for (int j = 0; j < kMaxStreams; j++) {
     cudaStreamDestroy(h->ls[j]);
-    cudaStreamDestroy(h->q[j]);
+    cudaEventDestroy(h->fjoin[j]);
     cudaEventDestroy(h->ls_done[j]);
     cudaEventDestroy(h->done[j]);
     cudaEventDestroy(h->joins[j]);
   }
   cudaEventDestroy(h->sh_done);
+  for (int j = 0; j < 2 * kMaxStreams + 1; j++) cudaStreamDestroy(h->q[j]);
   cudaEventDestroy(h->staged);
   for (auto& ev : h->ev) cudaEventDestroy(ev);
   cudaEventDestroy(h->fork);

@@ -217,11 +217,34 @@ __device__ __forceinline__ void wots_leaf(const KeyDev& K, uint32_t layer, uint6
   TStream<V> ts;
   ts.begin(mid, make_adrs(layer, tree, ADDR_WOTS_PK, leaf, 0, 0), column, stride);
   Adrs wa = make_adrs(layer, tree, ADDR_WOTS, leaf, 0, 0);
+  // The chain secrets PRF(SK.seed, ADRS(chain i, hash 0)) of one leaf differ
+  // only in ADRS word 4 (the chain index): SHA-256 rounds [0, NW+4) are run
+  // once per leaf and kept in this thread's smem column (words 32..39).
+  {
+    uint32_t W[NW + 4], s[8];
+#pragma unroll
+    for (int j = 0; j < NW; j++) W[j] = sks[j];
+    W[NW + 0] = wa.w0; W[NW + 1] = wa.w1; W[NW + 2] = wa.w2; W[NW + 3] = wa.w3;
+#pragma unroll
+    for (int j = 0; j < 8; j++) s[j] = IVc(j);
+    rounds_prefix<V, NW + 4>(s, W);
+#pragma unroll
+    for (int j = 0; j < 8; j++) column[(32 + j) * stride] = s[j];
+  }
 #pragma unroll 1
   for (int i = 0; i < Pr::wots_len; i++) {
-    uint32_t st[8];
+    uint32_t st[8], sR[8], W[16];
     adrs_set_chain_hash(wa, (uint32_t)i, 0);
-    prf_reg<V, NW>(st, sks, wa);
+#pragma unroll
+    for (int j = 0; j < NW; j++) W[j] = sks[j];
+    W[NW + 0] = wa.w0; W[NW + 1] = wa.w1; W[NW + 2] = wa.w2; W[NW + 3] = wa.w3; W[NW + 4] = wa.w4;
+    W[NW + 5] = 0x8000u;  // hash index 0, then the padding bit
+#pragma unroll
+    for (int j = NW + 6; j < 15; j++) W[j] = 0;
+    W[15] = (uint32_t)((4 * NW + 22) * 8);
+#pragma unroll
+    for (int j = 0; j < 8; j++) { st[j] = IVc(j); sR[j] = column[(32 + j) * stride]; }
+    compress_resume<V, NW + 4>(st, sR, W);
     uint32_t x[NW];
 #pragma unroll
     for (int j = 0; j < NW; j++) x[j] = st[j];
@@ -243,6 +266,7 @@ __device__ __forceinline__ void wots_leaf(const KeyDev& K, uint32_t layer, uint6
 // consecutive lanes of one warp and are reduced with shuffles.
 // ---------------------------------------------------------------------------
 constexpr int kTreeBlock = 128;
+constexpr int kLeafColumnWords = 40;  // per-thread smem column: 32-word T_len ring + 8-word PRF prefix
 #ifndef HS_TREE_MIN_BLOCKS
 #define HS_TREE_MIN_BLOCKS 5
 #endif
@@ -253,7 +277,7 @@ template <int S, class V>
 __global__ void __launch_bounds__(kTreeBlock, (S == 2 ? 4 : kTreeMinBlocks)) tree_sign_kernel(LaunchArgs a) {
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
-  __shared__ uint32_t tbuf[32 * kTreeBlock];
+  __shared__ uint32_t tbuf[kLeafColumnWords * kTreeBlock];
   // layers >= d - shared_layers come from the shared-subtree table instead
   const uint64_t per_msg = (uint64_t)(Pr::d - a.shared_layers) * Pr::leaves;
   const uint64_t gid = (uint64_t)blockIdx.x * kTreeBlock + threadIdx.x;
@@ -341,7 +365,7 @@ __global__ void __launch_bounds__(kTreeBlock, (S == 2 ? 4 : kTreeMinBlocks)) tre
   using Pr = P<S>;
   using Sh = Shared<S>;
   constexpr int NW = Pr::NW;
-  __shared__ uint32_t tbuf[32 * kTreeBlock];
+  __shared__ uint32_t tbuf[kLeafColumnWords * kTreeBlock];
   const int U = Sh::units(a.shared_layers);
   const uint64_t per_key = (uint64_t)U * Pr::leaves;
   const uint64_t gid = (uint64_t)blockIdx.x * kTreeBlock + threadIdx.x;
@@ -731,7 +755,7 @@ template <int S, class V>
 __global__ void __launch_bounds__(kTreeBlock) keygen_root_kernel(LaunchArgs a) {
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
-  __shared__ uint32_t tbuf[32 * kTreeBlock];
+  __shared__ uint32_t tbuf[kLeafColumnWords * kTreeBlock];
   const uint64_t gid = (uint64_t)blockIdx.x * kTreeBlock + threadIdx.x;
   const bool valid = gid < (uint64_t)a.nkeys * Pr::leaves;
   const uint32_t key = valid ? (uint32_t)(gid / Pr::leaves) : 0u;
