@@ -1,0 +1,64 @@
+"""GPU edge cases: long and empty messages, extreme seeds, single-message and
+odd-sized batches, repeated batches through a captured graph."""
+
+from __future__ import annotations
+
+import random
+
+import pytest
+
+from conftest import SETS
+
+import paper_2512_23969_b200 as hs
+from paper_2512_23969_b200.params import derive
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eng():
+    return hs.get_engine()
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_long_and_empty_messages(eng, oracle_mod, set_id):
+    p = derive(set_id)
+    rng = random.Random(3)
+    sk = oracle_mod.keygen(set_id, rng.randbytes(3 * p.n))
+    msgs = [b"", rng.randbytes(5000), b"\x00", rng.randbytes(70001), rng.randbytes(64 * 7 - 9)]
+    eng.upload_keys(set_id, sk)
+    sigs = eng.sign_batch(set_id, msgs)
+    for m, s in zip(msgs, sigs):
+        assert s == oracle_mod.sign(set_id, sk, m)
+    assert all(eng.verify_batch(set_id, sk[2 * p.n:], msgs, sigs))
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_extreme_seeds(eng, oracle_mod, set_id):
+    p = derive(set_id)
+    seeds = [bytes(3 * p.n), b"\xff" * (3 * p.n)]
+    sks = eng.keygen_batch(set_id, seeds)
+    assert sks == [oracle_mod.keygen(set_id, s) for s in seeds]
+    eng.upload_keys(set_id, sks)
+    msgs = [b"\xff" * 33, bytes(32)]
+    sigs = eng.sign_batch(set_id, msgs, key_idx=[1, 0], opt_rand=[b"\xff" * p.n, bytes(p.n)])
+    assert sigs[0] == oracle_mod.sign(set_id, sks[1], msgs[0], b"\xff" * p.n)
+    assert sigs[1] == oracle_mod.sign(set_id, sks[0], msgs[1], bytes(p.n))
+
+
+@pytest.mark.parametrize("count", [1, 7, 257, 1031])
+def test_batch_sizes_and_graph_replay(eng, oracle_mod, count):
+    """Odd batch sizes (partial warps / blocks / sub-batches); the same shape twice
+    replays the captured graph and must give the same bytes."""
+    p = derive("128f")
+    rng = random.Random(count)
+    sk = oracle_mod.keygen("128f", rng.randbytes(48))
+    msgs = [rng.randbytes(32) for _ in range(count)]
+    eng.upload_keys("128f", sk)
+    first = eng.sign_batch("128f", msgs)
+    again = eng.sign_batch("128f", msgs)
+    assert first == again
+    check = sorted({0, count - 1, count // 2})
+    ref, _ = oracle_mod.sign_many("128f", sk, None, [msgs[i] for i in check])
+    assert [first[i] for i in check] == ref
+    assert all(eng.verify_batch("128f", sk[32:], msgs, first))
