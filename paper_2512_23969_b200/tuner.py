@@ -252,9 +252,10 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
                    tie_tolerance: float = 0.02, tune_variants: bool = True) -> dict:
     """Search the FORS layout and per-kernel SHA-256 path on this device.
 
-    1. ``device_candidates`` ranks layouts by Algorithm 1 at S_max = opt-in smem;
-       the ``top`` ranked plus the best of each Relax mode are timed (FORS_Sign
-       kernel, CUDA events, serial mode) and the fastest trimmed mean wins.
+    1. ``device_candidates`` enumerates every layout Algorithm 1 admits at
+       S_max = opt-in smem (both Relax modes); each is timed (FORS_Sign kernel,
+       CUDA events, serial mode), the ``top`` fastest are re-timed and the best
+       trimmed mean wins.
     2. For each kernel the 'imad' path replaces 'native' only if it is faster
        by more than ``tie_tolerance`` (the reference's rule, tuner.py:206-218).
     Returns the chosen config plus the timing table; the engine is left
@@ -262,16 +263,20 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
     """
     p = derive(set_id)
     info = engine.device_info()
-    cands = device_candidates(p, info["smem_optin"])
-    pick = list(cands[:top])
-    for relax in (False, True):
-        best_r = next((c for c in cands if c.relax == relax), None)
-        if best_r is not None and best_r not in pick:
-            pick.append(best_r)
+    # Every feasible layout (no alpha pruning: small CTAs that share an SM hide
+    # each other's sparse upper levels) is timed once; the `top` fastest are
+    # re-timed with `reps` runs and the best trimmed mean wins.
+    cands = device_candidates(p, info["smem_optin"], alpha=0.0)
     _synthetic(engine, set_id, count)
     base = engine.config(set_id)
+    first = []
+    for c in cands:
+        engine.set_config(set_id, fors_trees_per_set=c.trees_per_set, fors_sets_fused=c.sets_fused,
+                          fors_relax=c.relax)
+        first.append((min(_kernel_ms(engine, set_id, count, "FORS_Sign", 2)), c))
+    first.sort(key=lambda x: x[0])
     table = []
-    for c in pick:
+    for _, c in first[:top]:
         engine.set_config(set_id, fors_trees_per_set=c.trees_per_set, fors_sets_fused=c.sets_fused,
                           fors_relax=c.relax)
         ms = _trimmed_mean(_kernel_ms(engine, set_id, count, "FORS_Sign", reps))
