@@ -120,14 +120,20 @@ void run(const char* name, int cap_blocks = 0) {
 
 int main() {
   setvbuf(stdout, NULL, _IONBF, 0);
-  run<Native, 1>("Native");
-  run<Fast, 1>("Fast (cbank)");
-  run<FastR, 1>("FastR (register consts)");
-  run<Native, 1, 128, 6>("Native", 5);
-  run<Fast, 1, 128, 6>("Fast", 5);
-  run<FastR, 1, 128, 6>("FastR", 5);
+  //                               NS1 NS0 NSS SHR T1F ANF WF
   run<Native, 1, 128, 8>("Native", 4);
-  run<Fast, 1, 128, 8>("Fast", 4);
-  run<FastR, 1, 128, 8>("FastR", 4);
+  run<Fast, 1, 128, 8>("Fast 000S1A-", 4);
+  run<Mix<0, 0, 0, true, 0, false, false>, 1, 128, 8>("Mix 000S0--", 4);
+  run<Mix<0, 0, 0, false, 1, false, false>, 1, 128, 8>("Mix 000-1--", 4);
+  run<Mix<0, 0, 0, false, 0, true, false>, 1, 128, 8>("Mix 000-0A-", 4);
+  run<Mix<0, 0, 0, true, 0, true, false>, 1, 128, 8>("Mix 000S0A-", 4);
+  run<Mix<0, 0, 0, false, 1, true, false>, 1, 128, 8>("Mix 000-1A-", 4);
+  run<Mix<0, 0, 0, true, 1, false, false>, 1, 128, 8>("Mix 000S1--", 4);
+  run<Native, 1, 128, 6>("Native", 5);
+  run<Mix<0, 0, 0, true, 0, false, false>, 1, 128, 6>("Mix 000S0--", 5);
+  run<Mix<0, 0, 0, false, 1, false, false>, 1, 128, 6>("Mix 000-1--", 5);
+  run<Mix<0, 0, 0, false, 0, true, false>, 1, 128, 6>("Mix 000-0A-", 5);
+  run<Mix<0, 0, 0, true, 0, true, false>, 1, 128, 6>("Mix 000S0A-", 5);
+  run<Mix<0, 0, 0, false, 1, true, false>, 1, 128, 6>("Mix 000-1A-", 5);
   return 0;
 }
