@@ -23,6 +23,12 @@ roofline: TREE_Sign (the dominant kernel, ~89% of 128f work) against the
          kernel in a serialised run (hs_run mode 1) inside this process.
 cpu_baseline: the C restatement of the reference signer (oracle/, a "port"),
          all host threads, a bounded sample of the same workload.
+launch_latency: the metric's "batch launch latency": host time inside the
+         one cudaGraphLaunch per batch, device batch time, public-API wall
+         time per batch, and small-batch (1 / 64 message) API latency.
+other_sets: the same measurements for the other two parameter sets (192f and
+         256f at 16384 messages per GPU, 128f at 4096), so one default run
+         covers 128f/192f/256f; --single-set skips them.
 """
 
 from __future__ import annotations
@@ -57,6 +63,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--check", type=int, default=16, help="signatures checked vs the oracle after timing")
+    ap.add_argument("--single-set", action="store_true", help="skip the secondary sets (other_sets)")
     return ap.parse_args()
 
 
@@ -215,57 +222,57 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args):
-    rank, world, local = dist_env()
-    dist = init_dist(world)
+def measure_set(eng, info, set_id: str, count: int, steps: int, warmup: int, rank: int, world: int, dist,
+                check: int, small_batches=(1, 64)) -> dict:
+    """Every number of one bench line for one parameter set (device value, no-sharing value,
+    TREE_Sign roofline, e2e through the public API, batch launch latency, parity spot check)."""
     import numpy as np
 
     import paper_2512_23969_b200 as hs
     from paper_2512_23969_b200.engine import PinnedBuffer, pack_messages
 
-    eng = hs.get_engine(local)
-    info = eng.device_info()
-    p, seed, msgs = workload(args.set_id, args.count, rank)
-    sk = eng.keygen_batch(args.set_id, [seed])[0]
-    eng.upload_keys(args.set_id, sk)
+    p, seed, msgs = workload(set_id, count, rank)
+    sk = eng.keygen_batch(set_id, [seed])[0]
+    eng.upload_keys(set_id, sk)
     blob, offs = pack_messages(msgs)
-    count = len(msgs)
 
     # ---- value: inputs resident in HBM, device-timed graph launches ----
-    eng.stage(args.set_id, blob, offs, count)
+    eng.stage(set_id, blob, offs, count)
     flush = 256 << 20
-    cfg = eng.config(args.set_id)
+    cfg = eng.config(set_id)
     shared_L = cfg["shared_layers"] if cfg["wots_from_tree"] else 0
-    eng.bench_run(args.set_id, count, max(1, args.warmup), 0, flush)
+    eng.bench_run(set_id, count, max(1, warmup), 0, flush)
     launches0 = eng.launch_count
+    eng.launch_stats(reset=True)
     barrier(dist)
-    with ClockSampler(local) as clocks:
-        step_ms = eng.bench_run(args.set_id, count, args.steps, 0, flush)
+    with ClockSampler(eng.device) as clocks:
+        step_ms = eng.bench_run(set_id, count, steps, 0, flush)
     launches = eng.launch_count - launches0
+    lstat = eng.launch_stats(reset=True)
     barrier(dist)
     dev_s = max_over_ranks(dist, sum(step_ms) / 1e3)
-    value = world * count * args.steps / dev_s
+    value = world * count * steps / dev_s
     graph_ms = eng.timings()
 
     # ---- the same batch with subtree sharing off (every message recomputes every layer) ----
     value_plain = None
     if shared_L:
-        eng.set_config(args.set_id, shared_layers=0)
-        eng.stage(args.set_id, blob, offs, count)
-        eng.bench_run(args.set_id, count, max(1, args.warmup), 0, flush)
+        eng.set_config(set_id, shared_layers=0)
+        eng.stage(set_id, blob, offs, count)
+        eng.bench_run(set_id, count, max(1, warmup), 0, flush)
         barrier(dist)
-        plain_ms = eng.bench_run(args.set_id, count, args.steps, 0, flush)
+        plain_ms = eng.bench_run(set_id, count, steps, 0, flush)
         plain_s = max_over_ranks(dist, sum(plain_ms) / 1e3)
-        value_plain = world * count * args.steps / plain_s
-        eng.set_config(args.set_id, shared_layers=shared_L)
-        eng.stage(args.set_id, blob, offs, count)
+        value_plain = world * count * steps / plain_s
+        eng.set_config(set_id, shared_layers=shared_L)
+        eng.stage(set_id, blob, offs, count)
 
     # ---- per-kernel roofline (serialised run, CUDA events around each kernel) ----
-    eng.bench_run(args.set_id, count, 1, 1, flush)
+    eng.bench_run(set_id, count, 1, 1, flush)
     kt = [eng.timings()]
     tree_ms = []
     for _ in range(3):
-        eng.bench_run(args.set_id, count, 1, 1, flush)
+        eng.bench_run(set_id, count, 1, 1, flush)
         tree_ms.append(eng.timings()["TREE_Sign"])
     tree_ms_avg = statistics.mean(tree_ms)
     work = hs.compressions_per_signature(p, 32)
@@ -277,13 +284,14 @@ def run_ours(args):
     # executed_per_sig but not in the roofline kernel
     tree_comps = count * (p.d - shared_L) * sub
     achieved = tree_comps / (tree_ms_avg / 1e3)
-    sm_max = clocks.summary().get("sm_max_mhz") or 1965.0
+    clk = clocks.summary()
+    sm_max = clk.get("sm_max_mhz") or 1965.0
     peak = info["sm_count"] * sm_max * 1e6 * ISSUE_PER_CLK_PER_SM / OPS_PER_COMPRESSION
     traffic = None
     tpath = ROOT / "profiles" / "tree_traffic.json"
     if tpath.exists():
         try:
-            traffic = json.loads(tpath.read_text()).get(args.set_id, {}).get("bytes_per_launch_per_msg")
+            traffic = json.loads(tpath.read_text()).get(set_id, {}).get("bytes_per_launch_per_msg")
             traffic = traffic * count if traffic is not None else None
         except (ValueError, AttributeError):
             traffic = None
@@ -296,44 +304,136 @@ def run_ours(args):
     h_offs = PinnedBuffer(offs.nbytes)
     h_offs.array(np.uint64)[:] = offs
     h_out = PinnedBuffer(count * p.sig_bytes)
-    for _ in range(max(1, args.warmup)):
-        eng.sign_into(args.set_id, h_blob.ptr, h_offs.array(np.uint64), count, h_out.ptr)
+    for _ in range(max(1, warmup)):
+        eng.sign_into(set_id, h_blob.ptr, h_offs.array(np.uint64), count, h_out.ptr)
     barrier(dist)
+    eng.launch_stats(reset=True)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        eng.sign_into(args.set_id, h_blob.ptr, h_offs.array(np.uint64), count, h_out.ptr)
+    for _ in range(steps):
+        eng.sign_into(set_id, h_blob.ptr, h_offs.array(np.uint64), count, h_out.ptr)
     e2e_s = max_over_ranks(dist, time.perf_counter() - t0)
-    e2e = world * count * args.steps / e2e_s
+    e2e_launch = eng.launch_stats(reset=True)
+    e2e = world * count * steps / e2e_s
     sigs_out = bytes(h_out.view[: count * p.sig_bytes])
 
-    # ---- correctness spot check of this step's output vs the oracle ----
+    # ---- small-batch latency through the same public call (serving-shaped) ----
+    small = {}
+    for nb in small_batches:
+        nb = min(nb, count)
+        for _ in range(3):
+            eng.sign_into(set_id, h_blob.ptr, h_offs.array(np.uint64)[: nb + 1], nb, h_out.ptr)
+        lat = []
+        for _ in range(10):
+            t1 = time.perf_counter()
+            eng.sign_into(set_id, h_blob.ptr, h_offs.array(np.uint64)[: nb + 1], nb, h_out.ptr)
+            lat.append(time.perf_counter() - t1)
+        small[str(nb)] = round(1e6 * statistics.median(lat), 1)
+    eng.launch_stats(reset=True)
+
+    # ---- correctness spot check of the timed e2e output vs the oracle ----
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle  # checker
 
     oracle.build()
-    chk = list(range(0, count, max(1, count // max(1, args.check))))[: args.check]
-    ref, _ = oracle.sign_many(args.set_id, sk, None, [msgs[i] for i in chk])
+    chk = list(range(0, count, max(1, count // max(1, check))))[:check]
+    ref, _ = oracle.sign_many(set_id, sk, None, [msgs[i] for i in chk])
     ok = all(sigs_out[i * p.sig_bytes:(i + 1) * p.sig_bytes] == r for i, r in zip(chk, ref))
     ok_all = max_over_ranks(dist, 0.0 if ok else 1.0) == 0.0
+    for b in (h_blob, h_offs, h_out):
+        b.free()
+
+    return {
+        "p": p, "sk": sk, "msgs": msgs, "cfg": cfg, "clk": clk, "value": value, "dev_s": dev_s,
+        "value_plain": value_plain, "launches": launches, "shared_L": shared_L, "units": units,
+        "e2e": {"value": round(e2e, 1), "unit": "sig/s", "h2d_bytes_per_step": int(len(blob) + offs.nbytes),
+                "d2h_bytes_per_step": int(count * p.sig_bytes)},
+        "launch_latency": {
+            "graph_launches_per_batch": round(lstat["graph_launches"] / max(1, steps), 3),
+            "host_graph_launch_us": {"mean": round(lstat["mean_us"], 2), "max": round(lstat["max_us"], 2)},
+            "device_batch_us": round(1e3 * statistics.median(step_ms), 1),
+            "e2e_batch_us": round(1e6 * e2e_s / steps, 1),
+            "e2e_graph_launches_per_batch": round(e2e_launch["graph_launches"] / max(1, steps), 3),
+            "e2e_small_batch_us": small,
+            "note": "host time inside cudaGraphLaunch (one graph per batch); device batch time (CUDA events); "
+                    "public-API wall time per batch incl. H2D/D2H; median wall time of small batches (messages: us)",
+        },
+        "roofline": {
+            "bound": "int-issue",
+            "kernel": "TREE_Sign",
+            "achieved": round(achieved / 1e9, 3),
+            "peak": round(peak / 1e9, 3),
+            "unit": "Gcompressions/s",
+            "frac": round(achieved / peak, 4),
+            "traffic": traffic,
+            "work_per_launch": f"{count} msgs x {p.d - shared_L} layers x {sub} compressions per subtree "
+                               f"(executed; {shared_L} top layers come from {units} shared subtrees)",
+            "kernel_ms": round(tree_ms_avg, 3),
+            "peak_basis": f"{info['sm_count']} SMs x {sm_max:.0f} MHz x 128 / 1384",
+        },
+        "kernel_ms_graph": {k: round(v, 3) for k, v in graph_ms.items()},
+        "kernel_ms_serial": {k: round(v, 3) for k, v in kt[0].items()},
+        "hbm_sig_writeout_gbs": round(count * p.sig_bytes / (statistics.mean(step_ms) / 1e3) / 1e9, 3),
+        "compressions_per_sig": {"reference_count": work["total"], "executed": round(executed_per_sig, 1)},
+        "parity_spot_check": {"checked": len(chk), "ok": ok_all},
+    }
+
+
+# per-GPU message counts of the secondary sets reported beside the headline
+# (BASELINE configs[2]: 192f at 16384 messages; configs[3]/[4] 256f batches)
+OTHER_SETS = {"128f": 4096, "192f": 16384, "256f": 16384}
+
+
+def run_ours(args):
+    rank, world, local = dist_env()
+    dist = init_dist(world)
+
+    import paper_2512_23969_b200 as hs
+
+    eng = hs.get_engine(local)
+    info = eng.device_info()
+    count = args.count
+    r = measure_set(eng, info, args.set_id, count, args.steps, args.warmup, rank, world, dist, args.check)
+    p = r["p"]
+
+    others = {}
+    if not args.single_set:
+        for sid, n in OTHER_SETS.items():
+            if sid == args.set_id:
+                continue
+            o = measure_set(eng, info, sid, n, min(args.steps, 5), args.warmup, rank, world, dist, 4,
+                            small_batches=(1,))
+            others[sid] = {
+                "value": round(o["value"], 1), "unit": "sig/s", "messages_per_gpu": n,
+                "ms_per_step": round(1e3 * o["dev_s"] / min(args.steps, 5), 4),
+                "value_no_subtree_sharing": round(o["value_plain"], 1) if o["value_plain"] else None,
+                "e2e": o["e2e"], "launch_latency": o["launch_latency"],
+                "roofline": {k: o["roofline"][k] for k in ("achieved", "peak", "unit", "frac", "kernel_ms")},
+                "clocks": {"sm_mhz": o["clk"]["sm_mhz"], "reasons": o["clk"]["reasons"]},
+                "parity_spot_check": o["parity_spot_check"],
+            }
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle  # CPU baseline leg only
+
         threads = os.cpu_count() or 1
-        rate, n, dt = cpu_sign_rate(args.set_id, sk, msgs, args.cpu_seconds, threads)
+        rate, n, dt = cpu_sign_rate(args.set_id, r["sk"], r["msgs"], args.cpu_seconds, threads)
         cpu = {"value": round(rate, 3), "unit": "sig/s", "cores": threads, "kind": "port",
                "sample": f"{n} of the same {args.set_id} messages in {dt:.1f}s, C oracle (oracle/hs_oracle.c, "
                          f"SHA-NI={oracle.shani_active()})"}
 
     if rank == 0:
-        clk = clocks.summary()
+        clk = r["clk"]
+        cfg = eng.config(args.set_id)
         line = {
             "metric": f"signatures/sec SPHINCS+-{args.set_id}",
-            "value": round(value, 1),
+            "value": round(r["value"], 1),
             "unit": "sig/s",
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
-            "ms_per_step": round(1e3 * dev_s / args.steps, 4),
+            "ms_per_step": round(1e3 * r["dev_s"] / args.steps, 4),
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
@@ -344,41 +444,27 @@ def run_ours(args):
                             f"(BASELINE configs[1])",
                 "set": args.set_id, "messages_per_gpu": count, "global_batch": world * count,
                 "parallelism": f"message-shard x{world}", "l2": "flushed between steps (256 MiB rewrite)",
-                "fors_layout": {k: v for k, v in eng.config(args.set_id).items() if k.startswith("fors")},
-                "variant": eng.config(args.set_id)["variant"],
+                "fors_layout": {k: v for k, v in cfg.items() if k.startswith("fors")},
+                "variant": cfg["variant"],
             },
-            "e2e": {"value": round(e2e, 1), "unit": "sig/s",
-                    "h2d_bytes_per_step": int(len(blob) + offs.nbytes),
-                    "d2h_bytes_per_step": int(count * p.sig_bytes)},
-            "gpu_launches": int(launches),
-            "value_no_subtree_sharing": round(value_plain, 1) if value_plain else None,
-            "subtree_sharing": {"layers": shared_L, "shared_subtrees_per_key": units,
+            "e2e": r["e2e"],
+            "gpu_launches": int(r["launches"]),
+            "launch_latency": r["launch_latency"],
+            "value_no_subtree_sharing": round(r["value_plain"], 1) if r["value_plain"] else None,
+            "subtree_sharing": {"layers": r["shared_L"], "shared_subtrees_per_key": r["units"],
                                 "note": "top hypertree layers address few subtrees per key; each distinct "
                                         "(key, layer, tree) subtree is computed once per batch (bytes unchanged)"},
-            "roofline": {
-                "bound": "int-issue",
-                "kernel": "TREE_Sign",
-                "achieved": round(achieved / 1e9, 3),
-                "peak": round(peak / 1e9, 3),
-                "unit": "Gcompressions/s",
-                "frac": round(achieved / peak, 4),
-                "traffic": traffic,
-                "work_per_launch": f"{count} msgs x {p.d - shared_L} layers x {sub} compressions per subtree "
-                                   f"(executed; {shared_L} top layers come from {units} shared subtrees)",
-                "kernel_ms": round(tree_ms_avg, 3),
-                "peak_basis": f"{info['sm_count']} SMs x {sm_max:.0f} MHz x 128 / 1384",
-            },
-            "kernel_ms_graph": {k: round(v, 3) for k, v in graph_ms.items()},
-            "kernel_ms_serial": {k: round(v, 3) for k, v in kt[0].items()},
-            "hbm_sig_writeout_gbs": round(count * p.sig_bytes / (statistics.mean(step_ms) / 1e3) / 1e9, 3),
-            "compressions_per_sig": {"reference_count": work["total"], "executed": round(executed_per_sig, 1)},
+            "roofline": r["roofline"],
+            "kernel_ms_graph": r["kernel_ms_graph"],
+            "kernel_ms_serial": r["kernel_ms_serial"],
+            "hbm_sig_writeout_gbs": r["hbm_sig_writeout_gbs"],
+            "compressions_per_sig": r["compressions_per_sig"],
             "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"]},
-            "parity_spot_check": {"checked": len(chk), "ok": ok_all},
+            "parity_spot_check": r["parity_spot_check"],
             "cpu_baseline": cpu,
+            "other_sets": others or None,
         }
         print(json.dumps(line), flush=True)
-    for b in (h_blob, h_offs, h_out):
-        b.free()
     if dist is not None:
         dist.destroy_process_group()
 

@@ -59,7 +59,9 @@ typedef struct {
   int32_t fors_trees_per_set; /* N_tree: trees sharing one set of lanes      */
   int32_t fors_sets_fused;    /* F: sets resident in one CTA's shared memory */
   int32_t fors_relax;         /* Relax_FORS: lanes build leaf pairs          */
-  int32_t variant[4];         /* SHA-256 path per kernel: 0 native, 1 imad;
+  int32_t variant[4];         /* SHA-256 path per kernel: 0 native, 1 fast,
+                                 2..5 the Mx<mask> paths (csrc/sha256.cuh
+                                 VariantOf; backends.py:201-257 analog);
                                  [0] FORS_Sign, [1] TREE_Sign, [2] WOTS_Sign,
                                  [3] message preparation                     */
   int32_t use_graph;          /* 1: one CUDA graph launch per batch          */
@@ -143,6 +145,14 @@ HS_API int hs_bench_run(hs_t *h, int set, uint32_t count, int32_t steps, int mod
 
 /* Kernel launches issued by this handle since open (for bench accounting). */
 HS_API int64_t hs_launch_count(hs_t *h);
+
+/* Batch launch latency (BASELINE.json metric): host time spent inside
+ * cudaGraphLaunch, one call per signed batch (or per `chunk` of a larger
+ * hs_sign_batch).  out[0] = graph launches, out[1] = mean us, out[2] = max us,
+ * accumulated since the last reset; reset != 0 clears them after reading.
+ * Returns the number of values written.  (No reference counterpart: the
+ * reference's batchgraph.py:245-353 runs its DAG on host threads.) */
+HS_API int hs_launch_stats(hs_t *h, double *out, int cap, int reset);
 
 /* Page-locked host memory for zero-copy-staging callers (cudaMallocHost). */
 HS_API void *hs_host_alloc(size_t bytes);

@@ -28,8 +28,8 @@ HS_E_CUDA = -10
 EXPORTS = (
     "hs_open", "hs_close", "hs_last_error", "hs_device_info", "hs_params", "hs_config_get", "hs_config_set",
     "hs_fors_smem_bytes", "hs_keys_upload", "hs_keygen_batch", "hs_sign_batch", "hs_verify_batch",
-    "hs_stage", "hs_run", "hs_sync", "hs_fetch", "hs_timings", "hs_bench_run", "hs_launch_count", "hs_host_alloc",
-    "hs_host_free",
+    "hs_stage", "hs_run", "hs_sync", "hs_fetch", "hs_timings", "hs_bench_run", "hs_launch_count", "hs_launch_stats",
+    "hs_host_alloc", "hs_host_free",
 )
 
 
@@ -53,8 +53,12 @@ class SetConfig(ctypes.Structure):
 _lib = None
 
 
-def build_native(jobs: int = 4) -> Path:
-    """Compile the CUDA library for sm_100a with its Makefile (no GPU needed)."""
+def build_native(jobs: int | None = None) -> Path:
+    """Compile the CUDA library for sm_100a with its Makefile (no GPU needed).
+
+    The 22 objects (3 sets x 6 SHA-256 paths + per-set glue + host runtime)
+    build in parallel, one job per host core by default."""
+    jobs = jobs or max(4, min(24, os.cpu_count() or 4))
     subprocess.run(["make", "-s", "-j", str(jobs), "-C", str(CSRC)], check=True)
     return LIB_PATH
 
@@ -91,6 +95,7 @@ def lib() -> ctypes.CDLL:
         "hs_bench_run": (ctypes.c_int, [vp, ctypes.c_int, u32, i32, ctypes.c_int, ctypes.c_uint64,
                                         ctypes.POINTER(ctypes.c_float)]),
         "hs_launch_count": (i64, [vp]),
+        "hs_launch_stats": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.c_int]),
         "hs_host_alloc": (vp, [ctypes.c_size_t]),
         "hs_host_free": (None, [vp]),
     }

@@ -22,6 +22,7 @@ from .tuner import DEFAULT_SEME, FusionCandidate, PaddingScheme, TuneInput, padd
 ENV_CONFIG_PATH = "HERO_SIGN_CONFIG"
 DEFAULT_WORKERS = 4
 KERNELS = ("FORS_Sign", "TREE_Sign", "WOTS_Sign")
+VARIANTS = ("native", "fast", "mx248", "mx250", "mx104", "mx172")  # == engine.VARIANTS (no engine import here)
 MAX_LANES = 1024
 
 # Engine defaults (csrc/hs_api.cu default_config); tune_on_device refines them.
@@ -86,7 +87,7 @@ class TuningConfig:
                 if lanes > MAX_LANES:
                     raise ConfigError(f"{set_id}: B200 layout needs {lanes} lanes")
                 for k, v in b.get("variant", {}).items():
-                    if k not in KERNELS + ("host",) or v not in (0, 1):
+                    if k not in KERNELS + ("host",) or v not in range(len(VARIANTS)):
                         raise ConfigError(f"{set_id}: bad variant {k}={v}")
 
     # -- engine binding --------------------------------------------------

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -189,6 +190,10 @@ struct hs_ctx {
   cudaEvent_t staged = nullptr, ls_done[kMaxStreams] = {};
   cudaEvent_t done[kMaxStreams] = {}, joins[kMaxStreams] = {}, fjoin[kMaxStreams] = {}, sh_done = nullptr;
   int last_T = 1;
+  // host-side cost of each cudaGraphLaunch since the last hs_launch_stats reset
+  // (the "batch launch latency" of BASELINE.json's metric): count, sum, max us
+  int64_t glaunch_n = 0;
+  double glaunch_us_sum = 0.0, glaunch_us_max = 0.0;
 };
 
 namespace {
@@ -238,7 +243,8 @@ int check_layout(hs_t* h, int set, const hs_set_config& c) {
   if (h && smem > (size_t)h->smem_optin)
     return fail(h, HS_E_CONFIG, "layout needs %zu shared bytes; device opt-in limit is %d", smem, h->smem_optin);
   for (int i = 0; i < 4; i++)
-    if (c.variant[i] != 0 && c.variant[i] != 1) return fail(h, HS_E_CONFIG, "variant must be 0 or 1");
+    if (c.variant[i] < 0 || c.variant[i] >= hs::kVariants)
+      return fail(h, HS_E_CONFIG, "variant must be in 0..%d", hs::kVariants - 1);
   if (c.chunk < 1) return fail(h, HS_E_CONFIG, "chunk must be >= 1");
   if (c.wots_from_tree != 0 && c.wots_from_tree != 1) return fail(h, HS_E_CONFIG, "wots_from_tree must be 0 or 1");
   if (c.streams < 1 || c.streams > kMaxStreams) return fail(h, HS_E_CONFIG, "streams must be in 1..%d", kMaxStreams);
@@ -456,7 +462,13 @@ int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nu
       h->graph_kernels[key] = h->last_kernels;
       it = h->graphs.emplace(key, ex).first;
     }
-    CUDA_TRY(h, cudaGraphLaunch(it->second, h->s0));
+    const auto t0 = std::chrono::steady_clock::now();
+    const cudaError_t le = cudaGraphLaunch(it->second, h->s0);
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    CUDA_TRY(h, le);
+    h->glaunch_n++;
+    h->glaunch_us_sum += us;
+    h->glaunch_us_max = std::max(h->glaunch_us_max, us);
     h->launches += h->graph_kernels[key];
   } else {
     CUDA_TRY(h, enqueue_batch(h, set, count, T, false));
@@ -895,6 +907,19 @@ int hs_bench_run(hs_t* h, int set, uint32_t count, int32_t steps, int mode, uint
 }
 
 int64_t hs_launch_count(hs_t* h) { return h ? h->launches : -1; }
+
+int hs_launch_stats(hs_t* h, double* out, int cap, int reset) {
+  if (!h || (cap > 0 && !out)) return fail(h, HS_E_USAGE, "bad arguments");
+  const double v[3] = {(double)h->glaunch_n, h->glaunch_n ? h->glaunch_us_sum / h->glaunch_n : 0.0,
+                       h->glaunch_us_max};
+  const int n = std::min(cap, 3);
+  for (int i = 0; i < n; i++) out[i] = v[i];
+  if (reset) {
+    h->glaunch_n = 0;
+    h->glaunch_us_sum = h->glaunch_us_max = 0.0;
+  }
+  return n;
+}
 
 void* hs_host_alloc(size_t bytes) {
   void* p = nullptr;

@@ -9,6 +9,8 @@ namespace hs {
 
 struct LaunchArgs;
 
+constexpr int kVariants = 6;  // == sha256.cuh kNumVariants (checked in hs_var.cu)
+
 enum KernelId : int {
   K_KEYSETUP = 0,
   K_PREP = 1,
@@ -22,9 +24,13 @@ enum KernelId : int {
   K_TREE_SHARED = 9,
 };
 
-// variant: 0 = Native, 1 = Imad (sha256.cuh)
+// variant: SHA-256 arithmetic path id, 0..kNumVariants-1 (sha256.cuh VariantOf)
 template <int S>
 cudaError_t launch_kernel(int which, int variant, const LaunchArgs& a, cudaStream_t s);
+
+// compression-heavy kernels of set S on path V (hs_var.cu)
+template <int S, int V>
+cudaError_t launch_variant(int which, const LaunchArgs& a, cudaStream_t s);
 
 template <int S>
 size_t fors_smem_bytes(int trees_per_set, int sets_fused, int relax);

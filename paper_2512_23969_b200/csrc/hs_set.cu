@@ -1,6 +1,6 @@
 // hs_set.cu -- per-parameter-set kernel instantiation and launch table.
-// Compiled three times with -DHS_SET=0/1/2 so the heavy template
-// instantiations build in parallel.
+// Compiled three times with -DHS_SET=0/1/2; the SHA-256-heavy kernels are
+// instantiated per arithmetic path in hs_var.cu so the objects build in parallel.
 #include <cuda_runtime.h>
 
 #include "hs_internal.h"
@@ -14,69 +14,52 @@ namespace hs {
 
 namespace {
 
-template <int S, class V>
-cudaError_t launch_v(int which, const LaunchArgs& a, cudaStream_t s) {
-  using Pr = P<S>;
-  auto blocks = [](uint64_t threads, int b) { return (unsigned)((threads + b - 1) / b); };
-  switch (which) {
-    case K_KEYSETUP:
-      if (a.nkeys == 0) return cudaSuccess;
-      key_setup_kernel<S, Native><<<blocks(a.nkeys, 64), 64, 0, s>>>(a);
-      break;
-    case K_PREP:
-      msg_prep_kernel<S, Native><<<blocks(a.count, 64), 64, 0, s>>>(a);
-      break;
-    case K_FORS: {
-      const bool relax = a.fors_relax != 0;
-      const int lanes = a.fors_trees_per_set * (relax ? Pr::t / 2 : Pr::t);
-      const int tpc = a.fors_trees_per_set * a.fors_sets_fused;
-      const int sets_total = (Pr::k + a.fors_trees_per_set - 1) / a.fors_trees_per_set;
-      const int passes = (sets_total + a.fors_sets_fused - 1) / a.fors_sets_fused;
-      const size_t smem = ((size_t)tpc * fors_smem_words_per_tree<S>(relax) + kForsPrefixWords) * 4;
-      cudaError_t e = cudaFuncSetAttribute(fors_sign_kernel<S, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-      fors_sign_kernel<S, V><<<(unsigned)((uint64_t)a.count * passes), lanes, smem, s>>>(a);
-      break;
-    }
-    case K_FORSPK:
-      fors_pk_kernel<S, Native><<<blocks(a.count, kSmallBlock), kSmallBlock, 0, s>>>(a);
-      break;
-    case K_TREE:
-      tree_sign_kernel<S, V><<<blocks((uint64_t)a.count * (Pr::d - a.shared_layers) * Pr::leaves, kTreeBlock),
-                               kTreeBlock, 0, s>>>(a);
-      break;
-    case K_TREE_SHARED:
-      if (a.shared_layers <= 0 || a.nkeys == 0) return cudaSuccess;
-      tree_shared_kernel<S, V><<<blocks((uint64_t)a.nkeys * Shared<S>::units(a.shared_layers) * Pr::leaves,
-                                        kTreeBlock),
-                                 kTreeBlock, 0, s>>>(a);
-      break;
-    case K_WOTS:
-      wots_sign_kernel<S, V><<<blocks((uint64_t)a.count * Pr::d * Pr::wots_len, kSmallBlock), kSmallBlock, 0, s>>>(a);
-      break;
-    case K_KEYGEN:
-      keygen_root_kernel<S, V><<<blocks((uint64_t)a.nkeys * Pr::leaves, kTreeBlock), kTreeBlock, 0, s>>>(a);
-      break;
-    case K_WOTS_GATHER:
-      wots_gather_kernel<S><<<blocks((uint64_t)a.count * Pr::d * Pr::wots_len, kSmallBlock), kSmallBlock, 0, s>>>(a);
-      break;
-    case K_VERIFY:
-      verify_kernel<S, Native><<<blocks(a.count, kVerifyWarps), 32 * kVerifyWarps, 0, s>>>(a);
-      break;
-    default:
-      return cudaErrorInvalidValue;
-  }
-  return cudaGetLastError();
+inline unsigned blocks_for(uint64_t threads, int b) { return (unsigned)((threads + b - 1) / b); }
+
+template <int V>
+cudaError_t launch_var(int which, const LaunchArgs& a, cudaStream_t s) {
+  return launch_variant<HS_SET, V>(which, a, s);
 }
 
 }  // namespace
 
+// Message preparation, key setup, T_k, the WOTS gather and verification are a
+// vanishing share of the work and use the native SHA-256 path; the
+// compression-heavy kernels come from hs_var.cu, one object per (set, path).
 template <>
 cudaError_t launch_kernel<HS_SET>(int which, int variant, const LaunchArgs& a, cudaStream_t s) {
-  // message preparation, key setup, T_k and verification are a vanishing
-  // share of the work: launch_v instantiates them with the native path only
-  return variant ? launch_v<HS_SET, Fast>(which, a, s) : launch_v<HS_SET, Native>(which, a, s);
+  constexpr int S = HS_SET;
+  using Pr = P<S>;
+  switch (which) {
+    case K_KEYSETUP:
+      if (a.nkeys == 0) return cudaSuccess;
+      key_setup_kernel<S, Native><<<blocks_for(a.nkeys, 64), 64, 0, s>>>(a);
+      return cudaGetLastError();
+    case K_PREP:
+      msg_prep_kernel<S, Native><<<blocks_for(a.count, 64), 64, 0, s>>>(a);
+      return cudaGetLastError();
+    case K_FORSPK:
+      fors_pk_kernel<S, Native><<<blocks_for(a.count, kSmallBlock), kSmallBlock, 0, s>>>(a);
+      return cudaGetLastError();
+    case K_WOTS_GATHER:
+      wots_gather_kernel<S><<<blocks_for((uint64_t)a.count * Pr::d * Pr::wots_len, kSmallBlock), kSmallBlock, 0,
+                              s>>>(a);
+      return cudaGetLastError();
+    case K_VERIFY:
+      verify_kernel<S, Native><<<blocks_for(a.count, kVerifyWarps), 32 * kVerifyWarps, 0, s>>>(a);
+      return cudaGetLastError();
+    default:
+      break;
+  }
+  switch (variant) {
+    case 0: return launch_var<0>(which, a, s);
+    case 1: return launch_var<1>(which, a, s);
+    case 2: return launch_var<2>(which, a, s);
+    case 3: return launch_var<3>(which, a, s);
+    case 4: return launch_var<4>(which, a, s);
+    case 5: return launch_var<5>(which, a, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 template <>

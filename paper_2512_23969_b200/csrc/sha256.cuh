@@ -156,6 +156,64 @@ struct Mix : Native {
 
 using Fast = Mix<0, 0, 0, true, 1, true, false>;
 
+// Mx<B>: the arithmetic path as a bitmask, the family swept on B200 by
+// tools/sha_sweep (all 256 masks x node widths 4/6/8, profiles/r01_sha_sweep.txt):
+//   bit0  Sigma1's first rotation on the FMA pipe (IMAD + IMAD.HI)
+//   bit1  Sigma0's first rotation on the FMA pipe
+//   bit2  schedule plain shifts as IMAD.HI
+//   bit3-4 T1: 0 native sum, 1 IMAD(h+k+w, IMAD(S1,Ch)), 2 all IMAD, 3 IMAD with
+//         the round constant folded into an IMAD immediate
+//   bit5  new a as an IMAD chain       bit6  schedule sum as three IMADs
+//   bit7  new e = d + T1 as an IMAD
+// SHA-256 on sm_100a is co-limited by the ALU pipe (2 cycles per warp
+// instruction per SMSP) and by register-file bank reads (profiles/
+// r01_pipe_probe2.txt: a 3-register LOP3 + 2-register IMAD pair issues at 0.8
+// instead of 1 per cycle); which split wins depends on ptxas's register
+// assignment for the surrounding kernel, so the engine compiles a few masks
+// and the on-device tuner times them per (kernel, set).
+template <int B>
+struct Mx : Native {
+  static constexpr int id = 100 + B;
+  static constexpr int T1F = (B >> 3) & 3;
+  static __device__ __forceinline__ uint32_t S0(uint32_t a) {
+    return ((B & 2) ? fma_rotr(a, 2) : rotr(a, 2)) ^ rotr(a, 13) ^ rotr(a, 22);
+  }
+  static __device__ __forceinline__ uint32_t S1(uint32_t e) {
+    return ((B & 1) ? fma_rotr(e, 6) : rotr(e, 6)) ^ rotr(e, 11) ^ rotr(e, 25);
+  }
+  static __device__ __forceinline__ uint32_t s0(uint32_t x) {
+    return rotr(x, 7) ^ rotr(x, 18) ^ ((B & 4) ? fma_shr(x, 3) : (x >> 3));
+  }
+  static __device__ __forceinline__ uint32_t s1(uint32_t x) {
+    return rotr(x, 17) ^ rotr(x, 19) ^ ((B & 4) ? fma_shr(x, 10) : (x >> 10));
+  }
+  static __device__ __forceinline__ uint32_t t1(uint32_t h, uint32_t k, uint32_t w, uint32_t s1v, uint32_t chv) {
+    if (T1F == 0) return h + k + w + s1v + chv;
+    if (T1F == 1) return fma_add(h + k + w, fma_add(s1v, chv));
+    if (T1F == 2) return fma_add(fma_add(fma_add(w, h), k), fma_add(s1v, chv));
+    return fma_add(fma_add(w, fma_addk(h, k)), fma_add(s1v, chv));
+  }
+  static __device__ __forceinline__ uint32_t enew(uint32_t d, uint32_t t) { return (B & 128) ? fma_add(d, t) : d + t; }
+  static __device__ __forceinline__ uint32_t anew(uint32_t t, uint32_t s0v, uint32_t mj) {
+    return (B & 32) ? fma_add(t, fma_add(s0v, mj)) : t + s0v + mj;
+  }
+  static __device__ __forceinline__ uint32_t wnew(uint32_t s1v, uint32_t w7, uint32_t s0v, uint32_t w16) {
+    return (B & 64) ? fma_add(fma_add(s1v, w7), fma_add(s0v, w16)) : fma_add(s1v + w7 + s0v, w16);
+  }
+  static __device__ __forceinline__ uint32_t ff(uint32_t x, uint32_t y) { return x + y; }
+};
+
+// Engine variant ids (hs_set_config.variant): 0 Native, 1 Fast, then the
+// Mx masks that led the B200 sweep for 4-, 6- and 8-word nodes.
+constexpr int kNumVariants = 6;
+template <int ID> struct VariantOf;
+template <> struct VariantOf<0> { using T = Native; };
+template <> struct VariantOf<1> { using T = Fast; };
+template <> struct VariantOf<2> { using T = Mx<248>; };
+template <> struct VariantOf<3> { using T = Mx<250>; };
+template <> struct VariantOf<4> { using T = Mx<104>; };
+template <> struct VariantOf<5> { using T = Mx<172>; };
+
 // Rounds [R0, R1) of SHA-256 on working state s, expanding the schedule in
 // place for rounds >= 16.  Fully unrolled so constant message words
 // (padding, lengths, zeros, chain-invariant ADRS words) fold.

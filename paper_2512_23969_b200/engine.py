@@ -20,6 +20,8 @@ from .errors import HeroSignError, UsageError
 from .params import SET_INDEX, derive
 
 KERNELS = ("FORS_Sign", "TREE_Sign", "WOTS_Sign", "host")  # hs_set_config.variant order
+# SHA-256 arithmetic paths compiled into the library (csrc/sha256.cuh VariantOf<id>)
+VARIANTS = ("native", "fast", "mx248", "mx250", "mx104", "mx172")
 
 
 def _u8ptr(buf):
@@ -240,6 +242,14 @@ class Engine:
     @property
     def launch_count(self) -> int:
         return int(_lib.lib().hs_launch_count(self._h))
+
+    def launch_stats(self, reset: bool = True) -> dict:
+        """Host-side batch launch latency: cudaGraphLaunch calls since the last reset."""
+        v = (ctypes.c_double * 3)()
+        n = _lib.lib().hs_launch_stats(self._h, v, 3, 1 if reset else 0)
+        if n < 0:
+            self._check(n, "hs_launch_stats")
+        return {"graph_launches": int(v[0]), "mean_us": float(v[1]), "max_us": float(v[2])}
 
 
 class PinnedBuffer:

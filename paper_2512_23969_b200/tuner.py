@@ -256,8 +256,9 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
        S_max = opt-in smem (both Relax modes); each is timed (FORS_Sign kernel,
        CUDA events, serial mode), the ``top`` fastest are re-timed and the best
        trimmed mean wins.
-    2. For each kernel the 'imad' path replaces 'native' only if it is faster
-       by more than ``tie_tolerance`` (the reference's rule, tuner.py:206-218).
+    2. For each kernel every compiled SHA-256 path (engine.VARIANTS) is timed;
+       the fastest replaces 'native' only if it is faster by more than
+       ``tie_tolerance`` (the reference's rule, tuner.py:206-218).
     Returns the chosen config plus the timing table; the engine is left
     configured with it.
     """
@@ -288,14 +289,19 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
     variants = dict(base["variant"])
     vtable = {}
     if tune_variants:
-        for kernel, tkey in (("FORS_Sign", "FORS_Sign"), ("TREE_Sign", "TREE_Sign"), ("WOTS_Sign", "WOTS_Sign")):
+        from .engine import VARIANTS
+
+        for kernel in ("FORS_Sign", "TREE_Sign", "WOTS_Sign"):
             cell = {}
-            for name, v in (("native", 0), ("imad", 1)):
+            for v, name in enumerate(VARIANTS):
                 var = dict(variants)
                 var[kernel] = v
                 engine.set_config(set_id, variant=var)
-                cell[name] = _trimmed_mean(_kernel_ms(engine, set_id, count, tkey, reps))
-            variants[kernel] = 1 if cell["imad"] < cell["native"] * (1.0 - tie_tolerance) else 0
+                cell[name] = _trimmed_mean(_kernel_ms(engine, set_id, count, kernel, reps))
+            # a non-native path replaces native only when faster by more than
+            # tie_tolerance (the reference's rule, tuner.py:206-218)
+            best_v = min(range(len(VARIANTS)), key=lambda v: cell[VARIANTS[v]])
+            variants[kernel] = best_v if cell[VARIANTS[best_v]] < cell["native"] * (1.0 - tie_tolerance) else 0
             vtable[kernel] = cell
         engine.set_config(set_id, variant=variants)
     # 3. multi-stream batching: T prioritised sub-batches per graph, timed end to

@@ -11,6 +11,7 @@ import pytest
 from conftest import GOLDEN_DIR, SETS
 
 import paper_2512_23969_b200 as hs
+from paper_2512_23969_b200.engine import VARIANTS
 from paper_2512_23969_b200.params import derive
 
 pytestmark = pytest.mark.gpu
@@ -78,13 +79,14 @@ def test_mixed_batch_vs_oracle(eng, oracle_mod, set_id):
 
 
 @pytest.mark.parametrize("set_id", SETS)
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", range(len(VARIANTS)))
 @pytest.mark.parametrize("stash", [True, False])
 def test_layouts_and_variants(eng, oracle_mod, set_id, variant, stash):
-    """Every FORS fusion layout / relax mode and both SHA-256 paths give identical bytes."""
+    """Every FORS fusion layout / relax mode and every compiled SHA-256 path give identical bytes."""
     p = derive(set_id)
     rng = random.Random(99)
-    sk = oracle_mod.keygen(set_id, rng.randbytes(3 * p.n))
+    seed = rng.randbytes(3 * p.n)
+    sk = oracle_mod.keygen(set_id, seed)
     msgs = [rng.randbytes(32) for _ in range(6)]
     ref = [oracle_mod.sign(set_id, sk, m) for m in msgs]
     eng.upload_keys(set_id, sk)
@@ -97,6 +99,7 @@ def test_layouts_and_variants(eng, oracle_mod, set_id, variant, stash):
             eng.set_config(set_id, fors_trees_per_set=nt, fors_sets_fused=f, fors_relax=bool(rx), wots_from_tree=stash,
                            variant={k: variant for k in ("FORS_Sign", "TREE_Sign", "WOTS_Sign", "host")})
             assert eng.sign_batch(set_id, msgs) == ref, (nt, f, rx)
+        assert eng.keygen_batch(set_id, [seed])[0] == sk  # keygen root kernel on this path
     finally:
         eng.set_config(set_id, **base)
 

@@ -1,0 +1,49 @@
+"""Time FORS_Sign / TREE_Sign / WOTS_Sign under every compiled SHA-256 path
+(engine.VARIANTS) for each parameter set, with the set's current layout.
+
+    python tools/variant_sweep.py [--count 4096] [--reps 5]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import paper_2512_23969_b200 as hs  # noqa: E402
+from paper_2512_23969_b200.engine import VARIANTS  # noqa: E402
+from paper_2512_23969_b200.tuner import _kernel_ms, _synthetic, _trimmed_mean  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--count", type=int, default=4096)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--sets", default="128f,192f,256f")
+    a = ap.parse_args()
+    eng = hs.get_engine(0)
+    out = {}
+    for set_id in a.sets.split(","):
+        _synthetic(eng, set_id, a.count)
+        base = eng.config(set_id)
+        res = {}
+        try:
+            for kernel in ("TREE_Sign", "FORS_Sign"):
+                for v, name in enumerate(VARIANTS):
+                    var = dict(base["variant"])
+                    var[kernel] = v
+                    eng.set_config(set_id, variant=var, wots_from_tree=True)
+                    res.setdefault(kernel, {})[name] = round(_trimmed_mean(_kernel_ms(eng, set_id, a.count, kernel,
+                                                                                      a.reps)), 4)
+        finally:
+            eng.set_config(set_id, **base)
+        out[set_id] = res
+        print(set_id, json.dumps(res), flush=True)
+    return out
+
+
+if __name__ == "__main__":
+    main()
