@@ -79,6 +79,13 @@ typedef struct {
                                  shareable subtrees are fewer than half the
                                  messages (and within the table budget);
                                  0: share exactly shared_layers              */
+  int32_t fors_cta_levels;    /* FORS tree levels reduced inside FORS_Sign's
+                                 CTA; the levels above run as batch-wide
+                                 one-level grids (fors_level_kernel).
+                                 0 = leaves only (1 with Relax), log_t =
+                                 whole tree in the CTA (reference shape,
+                                 vexec.py:437-463), -1 = auto (leaves only:
+                                 the measured best on B200)                  */
 } hs_set_config;
 
 HS_API int hs_open(int device, hs_t **out);
@@ -145,6 +152,13 @@ HS_API int hs_bench_run(hs_t *h, int set, uint32_t count, int32_t steps, int mod
 
 /* Kernel launches issued by this handle since open (for bench accounting). */
 HS_API int64_t hs_launch_count(hs_t *h);
+
+/* SHA-256 arithmetic paths compiled into this library (hs_set_config.variant
+ * ids): returns their number n; id 0 is the native path, id 1 the fast path,
+ * ids 2..n-1 are csrc/sha256.cuh Mx<mask> with masks[id-2] written to
+ * masks[0..min(cap, n-2)).  The paper's per-kernel PTX/native choice
+ * (reference backends.py:131-141 _COMPRESS registry) generalised. */
+HS_API int hs_variants(int32_t *masks, int cap);
 
 /* Batch launch latency (BASELINE.json metric): host time spent inside
  * cudaGraphLaunch, one call per signed batch (or per `chunk` of a larger

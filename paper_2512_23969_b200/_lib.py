@@ -15,7 +15,8 @@ from pathlib import Path
 from .errors import ConfigError, FormatError, HeroSignError, UsageError
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "libherosign_b200.so"
+# HERO_SIGN_LIB selects another build of the library (tools/variant_sweep.py)
+LIB_PATH = Path(os.environ["HERO_SIGN_LIB"]) if os.environ.get("HERO_SIGN_LIB") else PKG_DIR / "libherosign_b200.so"
 CSRC = PKG_DIR / "csrc"
 
 HS_OK = 0
@@ -28,7 +29,7 @@ HS_E_CUDA = -10
 EXPORTS = (
     "hs_open", "hs_close", "hs_last_error", "hs_device_info", "hs_params", "hs_config_get", "hs_config_set",
     "hs_fors_smem_bytes", "hs_keys_upload", "hs_keygen_batch", "hs_sign_batch", "hs_verify_batch",
-    "hs_stage", "hs_run", "hs_sync", "hs_fetch", "hs_timings", "hs_bench_run", "hs_launch_count", "hs_launch_stats",
+    "hs_stage", "hs_run", "hs_sync", "hs_fetch", "hs_timings", "hs_bench_run", "hs_launch_count", "hs_launch_stats", "hs_variants",
     "hs_host_alloc", "hs_host_free",
 )
 
@@ -47,6 +48,7 @@ class SetConfig(ctypes.Structure):
         ("streams", ctypes.c_int32),
         ("shared_layers", ctypes.c_int32),
         ("shared_auto", ctypes.c_int32),
+        ("fors_cta_levels", ctypes.c_int32),
     ]
 
 
@@ -96,6 +98,7 @@ def lib() -> ctypes.CDLL:
                                         ctypes.POINTER(ctypes.c_float)]),
         "hs_launch_count": (i64, [vp]),
         "hs_launch_stats": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.c_int]),
+        "hs_variants": (ctypes.c_int, [ctypes.POINTER(i32), ctypes.c_int]),
         "hs_host_alloc": (vp, [ctypes.c_size_t]),
         "hs_host_free": (None, [vp]),
     }
@@ -105,6 +108,14 @@ def lib() -> ctypes.CDLL:
         fn.argtypes = args
     _lib = L
     return L
+
+
+def variant_names() -> tuple[str, ...]:
+    """Names of the SHA-256 paths compiled into the loaded library (hs_variants):
+    ("native", "fast", "mx<mask>", ...), indexed by hs_set_config.variant id."""
+    buf = (ctypes.c_int32 * 64)()
+    n = lib().hs_variants(buf, 64)
+    return ("native", "fast") + tuple(f"mx{buf[i]}" for i in range(n - 2))
 
 
 def check(handle, rc: int, what: str) -> None:

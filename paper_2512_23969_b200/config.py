@@ -22,7 +22,7 @@ from .tuner import DEFAULT_SEME, FusionCandidate, PaddingScheme, TuneInput, padd
 ENV_CONFIG_PATH = "HERO_SIGN_CONFIG"
 DEFAULT_WORKERS = 4
 KERNELS = ("FORS_Sign", "TREE_Sign", "WOTS_Sign")
-VARIANTS = ("native", "fast", "mx248", "mx250", "mx104", "mx172")  # == engine.VARIANTS (no engine import here)
+MAX_VARIANTS = 64  # variant ids are checked against the built library by hs_config_set
 MAX_LANES = 1024
 
 # Engine defaults (csrc/hs_api.cu default_config); tune_on_device refines them.
@@ -87,7 +87,7 @@ class TuningConfig:
                 if lanes > MAX_LANES:
                     raise ConfigError(f"{set_id}: B200 layout needs {lanes} lanes")
                 for k, v in b.get("variant", {}).items():
-                    if k not in KERNELS + ("host",) or v not in range(len(VARIANTS)):
+                    if k not in KERNELS + ("host",) or not (isinstance(v, int) and 0 <= v < MAX_VARIANTS):
                         raise ConfigError(f"{set_id}: bad variant {k}={v}")
 
     # -- engine binding --------------------------------------------------
@@ -97,7 +97,7 @@ class TuningConfig:
             b = dict(cfg.b200) if cfg.b200 else {}
             kw = {}
             for key in ("fors_trees_per_set", "fors_sets_fused", "fors_relax", "wots_from_tree", "chunk", "streams",
-                        "shared_layers", "shared_auto"):
+                        "shared_layers", "shared_auto", "fors_cta_levels"):
                 if key in b:
                     kw[key] = b[key]
             if "variant" in b:
@@ -116,6 +116,7 @@ class TuningConfig:
                 "fors_relax": e["fors_relax"], "variant": {k: e["variant"][k] for k in KERNELS},
                 "wots_from_tree": e["wots_from_tree"], "chunk": e["chunk"], "streams": e["streams"],
                 "shared_layers": e["shared_layers"], "shared_auto": e["shared_auto"],
+                "fors_cta_levels": e["fors_cta_levels"],
             }
             cfg.sets[set_id].backends = {k: "tuned" if e["variant"][k] else "baseline" for k in KERNELS}
         return cfg

@@ -103,6 +103,7 @@ hs_set_config default_config(int set) {
   c.streams = 2;
   c.shared_layers = shared_max(set);
   c.shared_auto = 1;
+  c.fors_cta_levels = -1;
   return c;
 }
 
@@ -141,6 +142,7 @@ struct Buffers {
   uint32_t* stash = nullptr; size_t stash_cap = 0;
   uint32_t* shared = nullptr; size_t shared_cap = 0;   // subtree-sharing table
   uint8_t* key_used = nullptr; size_t key_used_cap = 0;
+  uint32_t* fnodes[2] = {nullptr, nullptr}; size_t fnodes_cap[2] = {0, 0};  // upper FORS levels
   // pinned staging
   uint8_t* h_msgs = nullptr; size_t h_msgs_cap = 0;
   uint64_t* h_offs = nullptr; size_t h_offs_cap = 0;
@@ -251,6 +253,8 @@ int check_layout(hs_t* h, int set, const hs_set_config& c) {
   if (c.shared_layers < 0 || c.shared_layers > shared_max(set))
     return fail(h, HS_E_CONFIG, "shared_layers must be in 0..%d for this set", shared_max(set));
   if (c.shared_auto != 0 && c.shared_auto != 1) return fail(h, HS_E_CONFIG, "shared_auto must be 0 or 1");
+  if (c.fors_cta_levels < -1 || c.fors_cta_levels > I.log_t)
+    return fail(h, HS_E_CONFIG, "fors_cta_levels must be -1 (auto) or in 0..%d", I.log_t);
   return HS_OK;
 }
 
@@ -274,6 +278,25 @@ int ensure_capacity(hs_t* h, int set, uint32_t count, size_t msg_bytes) {
     drop_graphs(h);
   }
   return HS_OK;
+}
+
+// FORS levels kept inside FORS_Sign's CTA (the rest run as one-level grids):
+// explicit 0..log_t (0: leaves only; with Relax the leaf phase already yields
+// level 1, so 0 means 1), or auto (-1): the measured best on B200 for every
+// tuned layout was to hand everything above the leaf phase to the grids
+// (tools/fors_split.py, profiles/r01_fors_split.txt).
+int fors_cta_levels(int set, const hs_set_config& c) {
+  const SetInfo& I = kInfo[set];
+  const int lowest = c.fors_relax ? 1 : 0;
+  if (c.fors_cta_levels < 0) return lowest;
+  return std::max(lowest, std::min(c.fors_cta_levels, I.log_t));
+}
+
+// words of fors_nodes[b]: buffer 0 holds levels Lc, Lc+2, ..., buffer 1 Lc+1, ...
+size_t fors_node_words(int set, const hs_set_config& c, uint32_t count, int b) {
+  const SetInfo& I = kInfo[set];
+  const int L = fors_cta_levels(set, c);
+  return L >= I.log_t ? 0 : (size_t)count * I.k * ((size_t)I.t >> (L + b)) * (I.n / 4);
 }
 
 // Arguments for messages [first, first + count) of the staged batch.  Message
@@ -300,6 +323,10 @@ LaunchArgs make_args(hs_t* h, int set, uint32_t first, uint32_t count) {
   a.fors_trees_per_set = St.cfg.fors_trees_per_set;
   a.fors_sets_fused = St.cfg.fors_sets_fused;
   a.fors_relax = St.cfg.fors_relax;
+  a.fors_cta_levels = fors_cta_levels(set, St.cfg);
+  if (a.fors_cta_levels < I.log_t)
+    for (int b = 0; b < 2; b++)
+      a.fors_nodes[b] = B.fnodes[b] + (size_t)first * I.k * ((size_t)I.t >> (a.fors_cta_levels + b)) * (I.n / 4);
   const size_t sw = stash_words(set);
   a.stash = (St.cfg.wots_from_tree && B.stash && B.stash_cap >= ((size_t)first + count) * sw)
                 ? B.stash + (size_t)first * sw
@@ -315,6 +342,36 @@ LaunchArgs make_args(hs_t* h, int set, uint32_t first, uint32_t count) {
   return a;
 }
 
+// FORS_Sign, the batch-wide upper FORS levels (if any) and T_k on one stream.
+cudaError_t enqueue_fors(int set, const hs_set_config& c, const LaunchArgs& a, cudaStream_t s, int& kernels) {
+  cudaError_t e = launch(set, K_FORS, c.variant[0], a, s);
+  kernels++;
+  for (int L = a.fors_cta_levels + 1; e == cudaSuccess && L <= kInfo[set].log_t; L++) {
+    LaunchArgs al = a;
+    al.fors_level = L;
+    e = launch(set, K_FORS_LEVEL, c.variant[0], al, s);
+    kernels++;
+  }
+  if (e == cudaSuccess) e = launch(set, K_FORSPK, c.variant[0], a, s);
+  kernels++;
+  return e;
+}
+
+// Upper-level FORS buffers for `count` messages under the current config.
+int ensure_fors_nodes(hs_t* h, int set, uint32_t count) {
+  Buffers& B = h->buf[set];
+  if (fors_node_words(set, h->sets[set].cfg, count, 0) == 0) return HS_OK;
+  void* before[2] = {B.fnodes[0], B.fnodes[1]};
+  for (int b = 0; b < 2; b++)
+    CUDA_TRY(h, grow(B.fnodes[b], B.fnodes_cap[b], fors_node_words(set, h->sets[set].cfg, count, b)));
+  void* after[2] = {B.fnodes[0], B.fnodes[1]};
+  if (std::memcmp(before, after, sizeof before) != 0) {
+    B.gen++;
+    drop_graphs(h);
+  }
+  return HS_OK;
+}
+
 // Issue the signing DAG.  `capture` selects external (graph-visible) timing
 // events; `serial` puts every kernel on s0 back to back.
 cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool serial) {
@@ -324,14 +381,13 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
   };
   cudaError_t e;
 #define TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
-  const int kernels = 5 + (a.shared_layers > 0 ? 1 : 0);
+  int kernels = 3 + (a.shared_layers > 0 ? 1 : 0);  // + the FORS branch, counted by enqueue_fors
   TRY(rec(0, h->s0));
   if (a.shared_layers > 0) TRY(cudaMemsetAsync(a.key_used, 0, a.nkeys, h->s0));
   TRY(launch(set, K_PREP, c.variant[3], a, h->s0));
   TRY(rec(1, h->s0));
   if (serial) {
-    TRY(launch(set, K_FORS, c.variant[0], a, h->s0));
-    TRY(launch(set, K_FORSPK, c.variant[0], a, h->s0));
+    TRY(enqueue_fors(set, c, a, h->s0, kernels));
     TRY(rec(2, h->s0));
     TRY(launch(set, K_TREE, c.variant[1], a, h->s0));
     TRY(rec(3, h->s0));  // [2,3] = per-message TREE_Sign only (the roofline kernel)
@@ -346,8 +402,7 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
     // one thread per leaf): start it first on the FORS branch so it runs
     // under the per-message TREE_Sign instead of after it
     if (a.shared_layers > 0) TRY(launch(set, K_TREE_SHARED, c.variant[1], a, h->s1));
-    TRY(launch(set, K_FORS, c.variant[0], a, h->s1));
-    TRY(launch(set, K_FORSPK, c.variant[0], a, h->s1));
+    TRY(enqueue_fors(set, c, a, h->s1, kernels));
     TRY(rec(2, h->s1));
     TRY(cudaEventRecord(h->join, h->s1));
     TRY(launch(set, K_TREE, c.variant[1], a, h->s0));
@@ -410,13 +465,12 @@ cudaError_t enqueue_batch(hs_t* h, int set, uint32_t count, int T, bool capture)
     TRY(cudaStreamWaitEvent(q, h->fork, 0));
     TRY(cudaStreamWaitEvent(qf, h->fork, 0));
     TRY(launch(set, K_TREE, c.variant[1], a, q));
-    TRY(launch(set, K_FORS, c.variant[0], a, qf));
-    TRY(launch(set, K_FORSPK, c.variant[0], a, qf));
+    TRY(enqueue_fors(set, c, a, qf, kernels));
     TRY(cudaEventRecord(h->fjoin[j], qf));
     TRY(cudaStreamWaitEvent(q, h->fjoin[j], 0));
     if (all.shared_layers > 0) TRY(cudaStreamWaitEvent(q, h->sh_done, 0));
     TRY(launch(set, a.stash ? K_WOTS_GATHER : K_WOTS, c.variant[2], a, q));
-    kernels += 4;
+    kernels += 2;
     TRY(rec(h->done[j], q));
     TRY(cudaEventRecord(h->joins[j], q));
     TRY(cudaStreamWaitEvent(h->s0, h->joins[j], 0));
@@ -434,6 +488,7 @@ int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nu
   h->last_set = set;
   h->last_mode = mode;
   const size_t sb = (size_t)kInfo[set].sig_bytes;
+  if (int rc = ensure_fors_nodes(h, set, std::max(count, St.staged)); rc != HS_OK) return rc;
   if (mode == 1) {  // serialised kernels with per-kernel events (roofline timing)
     CUDA_TRY(h, enqueue(h, set, make_args(h, set, 0, count), false, true));
     if (fetch_to)
@@ -622,6 +677,8 @@ void hs_close(hs_t* h) {
     cudaFree(h->sets[s].keys);
     cudaFree(B.shared);
     cudaFree(B.key_used);
+    cudaFree(B.fnodes[0]);
+    cudaFree(B.fnodes[1]);
     cudaFree(h->sets[s].sk_raw);
   }
   if (h->flush) cudaFree(h->flush);
@@ -907,6 +964,12 @@ int hs_bench_run(hs_t* h, int set, uint32_t count, int32_t steps, int mode, uint
 }
 
 int64_t hs_launch_count(hs_t* h) { return h ? h->launches : -1; }
+
+int hs_variants(int32_t* masks, int cap) {
+  const int nm = hs::kVariants - 2;
+  for (int i = 0; i < nm && i < cap; i++) masks[i] = hs::kMxMaskList[i];
+  return hs::kVariants;
+}
 
 int hs_launch_stats(hs_t* h, double* out, int cap, int reset) {
   if (!h || (cap > 0 && !out)) return fail(h, HS_E_USAGE, "bad arguments");

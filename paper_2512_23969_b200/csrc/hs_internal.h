@@ -5,11 +5,12 @@
 
 #include <cstddef>
 
+#include "hs_variants.h"
+
 namespace hs {
 
 struct LaunchArgs;
 
-constexpr int kVariants = 6;  // == sha256.cuh kNumVariants (checked in hs_var.cu)
 
 enum KernelId : int {
   K_KEYSETUP = 0,
@@ -22,6 +23,7 @@ enum KernelId : int {
   K_VERIFY = 7,
   K_WOTS_GATHER = 8,
   K_TREE_SHARED = 9,
+  K_FORS_LEVEL = 10,
 };
 
 // variant: SHA-256 arithmetic path id, 0..kNumVariants-1 (sha256.cuh VariantOf)

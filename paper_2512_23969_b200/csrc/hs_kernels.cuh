@@ -71,6 +71,13 @@ struct LaunchArgs {
   int fors_trees_per_set;    // N_tree
   int fors_sets_fused;       // F
   int fors_relax;
+  // FORS levels above fors_cta_levels are reduced by fors_level_kernel, one
+  // grid per level over every (message, tree, node); fors_nodes[0/1] hold the
+  // levels in between (node-major, NW words per node).  fors_cta_levels ==
+  // log_t keeps the whole tree inside the CTA (no level kernels).
+  int fors_cta_levels;
+  int fors_level;            // level computed by one fors_level_kernel launch
+  uint32_t* fors_nodes[2];
 };
 
 __device__ __forceinline__ uint64_t shr64(uint64_t x, int s) { return s >= 64 ? 0ull : (x >> s); }
@@ -253,7 +260,7 @@ __device__ __forceinline__ void wots_leaf(const KeyDev& K, uint32_t layer, uint6
 #pragma unroll
       for (int j = 0; j < NW; j++) crec[j] = x[j];
     }
-    chain_F<V, NW>(x, mid, wa, 0u, (uint32_t)(Pr::w - 1), crec);
+    chain_F_leaf<V, NW>(x, mid, wa, 0u, (uint32_t)(Pr::w - 1), crec);
     ts.template push_node<NW>(x);
   }
   ts.finish(22u + (uint32_t)(Pr::wots_len * Pr::n));
@@ -521,6 +528,12 @@ __global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) 
   __syncthreads();
 
   // ---- leaf phase (vexec.py:387-435) ----
+  // last = the level handed to fors_level_kernel through fors_nodes[0] (or
+  // log_t: the whole tree stays in this CTA).  With last == 0 (Relax: 1) the
+  // leaf phase writes its nodes straight to global memory and no level runs
+  // here at all.
+  const int last = a.fors_cta_levels;
+  const bool to_global = last == (relax ? 1 : 0);
   const int tree_in_set = tid / lanes_per_tree;
   const int lane_leaf = tid % lanes_per_tree;
 #pragma unroll 1
@@ -533,9 +546,15 @@ __global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) 
       uint32_t sk[8], lf[8];
       fors_leaf<S, V>(mid, sks, fa, pre, (uint32_t)(g * t + lane_leaf), sk, lf);
       if ((uint32_t)lane_leaf == sel) store_node<NW>(fsig + g * tree_sig, sk);
-      uint32_t* dst = regA + (size_t)tl * capA + lane_leaf;
+      if (to_global) {
+        uint32_t* d = a.fors_nodes[0] + (((size_t)msg * Pr::k + g) * t + lane_leaf) * NW;
 #pragma unroll
-      for (int j = 0; j < NW; j++) dst[(size_t)j * SA] = lf[j];
+        for (int j = 0; j < NW; j++) d[j] = lf[j];
+      } else {
+        uint32_t* dst = regA + (size_t)tl * capA + lane_leaf;
+#pragma unroll
+        for (int j = 0; j < NW; j++) dst[(size_t)j * SA] = lf[j];
+      }
     } else {
       uint32_t sk0[8], l0[8], sk1[8], l1[8];
       const uint32_t j2 = 2u * lane_leaf;
@@ -550,17 +569,24 @@ __global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) 
       Adrs pa = fa;
       adrs_set_chain_hash(pa, 1, (uint32_t)lane_leaf + ((uint32_t)(g * t) >> 1));
       thash_reg<V, 2 * NW>(par, mid, pa, m);
-      uint32_t* dst = regB + (size_t)tl * (t / 2) + lane_leaf;
+      if (to_global) {
+        uint32_t* d = a.fors_nodes[0] + (((size_t)msg * Pr::k + g) * (t / 2) + lane_leaf) * NW;
 #pragma unroll
-      for (int j = 0; j < NW; j++) dst[(size_t)j * SB] = par[j];
+        for (int j = 0; j < NW; j++) d[j] = par[j];
+      } else {
+        uint32_t* dst = regB + (size_t)tl * (t / 2) + lane_leaf;
+#pragma unroll
+        for (int j = 0; j < NW; j++) dst[(size_t)j * SB] = par[j];
+      }
     }
   }
+  if (to_global) return;  // uniform across the CTA
   __syncthreads();
 
   // ---- reduction levels (vexec.py:437-463) ----
   const int first = relax ? 2 : 1;
 #pragma unroll 1
-  for (int lvl = first; lvl <= Pr::log_t; lvl++) {
+  for (int lvl = first; lvl <= last; lvl++) {
     // level lvl-1 lives in A when (lvl-1) is even (no relax) ... track by parity
     const bool src_is_A = relax ? ((lvl & 1) == 1) : ((lvl & 1) == 1);
     const uint32_t* src = src_is_A ? regA : regB;
@@ -595,6 +621,10 @@ __global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) 
         uint32_t* r = a.fors_roots + ((size_t)msg * Pr::k + g) * 8;
 #pragma unroll
         for (int w = 0; w < NW; w++) r[w] = par[w];
+      } else if (lvl == last) {  // hand the sparse upper levels to fors_level_kernel
+        uint32_t* d = a.fors_nodes[0] + (((size_t)msg * Pr::k + g) * (uint32_t)per_tree + j) * NW;
+#pragma unroll
+        for (int w = 0; w < NW; w++) d[w] = par[w];
       } else {
         uint32_t* d = dst + (size_t)tl * dst_cap + j;
 #pragma unroll
@@ -603,6 +633,49 @@ __global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) 
     }
     __syncthreads();
   }
+}
+
+// One FORS level L > fors_cta_levels for the whole batch: thread = (message,
+// tree, node j of level L); children come from the level below in
+// fors_nodes[(L - Lc - 1) & 1], the parent goes to the other buffer (or to
+// fors_roots at the top).  Upper levels hold few nodes per tree, so inside a
+// CTA they leave most lanes idle at a barrier; as batch-wide grids every lane
+// has a node.  Same hash inputs and auth-path rule as the in-CTA levels
+// (vexec.py:437-463).
+constexpr int kForsLevelBlock = 128;
+template <int S, class V>
+__global__ void __launch_bounds__(kForsLevelBlock) fors_level_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  constexpr int NW = Pr::NW;
+  constexpr int t = Pr::t;
+  const int L = a.fors_level;
+  const uint32_t per_tree = (uint32_t)t >> L;
+  const uint64_t gid = (uint64_t)blockIdx.x * kForsLevelBlock + threadIdx.x;
+  if (gid >= (uint64_t)a.count * Pr::k * per_tree) return;
+  const uint32_t j = (uint32_t)(gid % per_tree);
+  const uint64_t tg = gid / per_tree;                  // msg * k + g
+  const uint32_t g = (uint32_t)(tg % Pr::k);
+  const uint32_t msg = (uint32_t)(tg / Pr::k);
+  const int par_buf = (L - a.fors_cta_levels) & 1;      // level Lc lives in buffer 0
+  const uint32_t* c = a.fors_nodes[par_buf ^ 1] + (tg * (2 * per_tree) + 2 * j) * NW;
+  uint32_t m[2 * NW];
+#pragma unroll
+  for (int w = 0; w < 2 * NW; w++) m[w] = c[w];
+  const MsgPlan pl = a.plans[msg];
+  const KeyDev& K = a.keys[pl.key];
+  const uint32_t sel = (uint32_t)a.indices[(size_t)msg * Pr::k + g] >> (L - 1);
+  constexpr int tree_sig = (1 + Pr::log_t) * Pr::n;
+  uint8_t* fsig = a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_fors;
+  if ((sel >> 1) == j) store_node<NW>(fsig + g * tree_sig + Pr::n + (L - 1) * Pr::n, (sel & 1u) ? m : m + NW);
+  uint32_t mid[8], par[8];
+#pragma unroll
+  for (int w = 0; w < 8; w++) mid[w] = K.thash_mid[w];
+  Adrs na = make_adrs(0, pl.tree, ADDR_FORS_TREE, pl.leaf, 0, 0);
+  adrs_set_chain_hash(na, (uint32_t)L, j + ((g * (uint32_t)t) >> L));
+  thash_reg<V, 2 * NW>(par, mid, na, m);
+  uint32_t* d = (L == Pr::log_t) ? a.fors_roots + tg * 8 : a.fors_nodes[par_buf] + (tg * per_tree + j) * NW;
+#pragma unroll
+  for (int w = 0; w < NW; w++) d[w] = par[w];
 }
 
 // T_k over the k FORS roots -> roots slot 0 (vexec.py:476-481).

@@ -17,8 +17,12 @@ namespace {
 inline unsigned blocks_for(uint64_t threads, int b) { return (unsigned)((threads + b - 1) / b); }
 
 template <int V>
-cudaError_t launch_var(int which, const LaunchArgs& a, cudaStream_t s) {
-  return launch_variant<HS_SET, V>(which, a, s);
+cudaError_t launch_var(int which, int variant, const LaunchArgs& a, cudaStream_t s) {
+  if constexpr (V >= kVariants) {
+    return cudaErrorInvalidValue;
+  } else {
+    return variant == V ? launch_variant<HS_SET, V>(which, a, s) : launch_var<V + 1>(which, variant, a, s);
+  }
 }
 
 }  // namespace
@@ -51,15 +55,7 @@ cudaError_t launch_kernel<HS_SET>(int which, int variant, const LaunchArgs& a, c
     default:
       break;
   }
-  switch (variant) {
-    case 0: return launch_var<0>(which, a, s);
-    case 1: return launch_var<1>(which, a, s);
-    case 2: return launch_var<2>(which, a, s);
-    case 3: return launch_var<3>(which, a, s);
-    case 4: return launch_var<4>(which, a, s);
-    case 5: return launch_var<5>(which, a, s);
-    default: return cudaErrorInvalidValue;
-  }
+  return launch_var<0>(which, variant, a, s);
 }
 
 template <>

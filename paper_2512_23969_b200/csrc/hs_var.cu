@@ -1,7 +1,7 @@
 // hs_var.cu -- the compression-heavy kernels (FORS_Sign, TREE_Sign, shared
 // subtrees, the WOTS chain kernel, keygen root) of one parameter set
 // instantiated for one SHA-256 arithmetic path (sha256.cuh VariantOf<ID>).
-// Compiled once per (HS_SET, HS_VAR) so the 18 objects build in parallel.
+// (+ the batch-wide upper FORS levels).  Compiled once per (HS_SET, HS_VAR) so the 18 objects build in parallel.
 #include <cuda_runtime.h>
 
 #include "hs_internal.h"
@@ -29,13 +29,20 @@ cudaError_t launch_variant<HS_SET, HS_VAR>(int which, const LaunchArgs& a, cudaS
       const int tpc = a.fors_trees_per_set * a.fors_sets_fused;
       const int sets_total = (Pr::k + a.fors_trees_per_set - 1) / a.fors_trees_per_set;
       const int passes = (sets_total + a.fors_sets_fused - 1) / a.fors_sets_fused;
-      const size_t smem = ((size_t)tpc * fors_smem_words_per_tree<S>(relax) + kForsPrefixWords) * 4;
+      // leaves-only CTAs (fors_cta_levels at its lowest) keep no tree levels in shared memory
+      const bool leaves_only = a.fors_cta_levels == (relax ? 1 : 0);
+      const size_t smem =
+          ((leaves_only ? 0 : (size_t)tpc * fors_smem_words_per_tree<S>(relax)) + kForsPrefixWords) * 4;
       cudaError_t e = cudaFuncSetAttribute(fors_sign_kernel<S, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
       if (e != cudaSuccess) return e;
       fors_sign_kernel<S, V><<<(unsigned)((uint64_t)a.count * passes), lanes, smem, s>>>(a);
       break;
     }
+    case K_FORS_LEVEL:
+      fors_level_kernel<S, V><<<blocks((uint64_t)a.count * Pr::k * ((uint32_t)Pr::t >> a.fors_level), kForsLevelBlock),
+                                kForsLevelBlock, 0, s>>>(a);
+      break;
     case K_TREE:
       tree_sign_kernel<S, V><<<blocks((uint64_t)a.count * (Pr::d - a.shared_layers) * Pr::leaves, kTreeBlock),
                                kTreeBlock, 0, s>>>(a);

@@ -21,6 +21,8 @@
 #pragma once
 #include <cstdint>
 
+#include "hs_variants.h"
+
 namespace hs {
 
 static __constant__ uint32_t c_one = 1u;  // opaque multiplicative identity (Imad path)
@@ -203,16 +205,13 @@ struct Mx : Native {
   static __device__ __forceinline__ uint32_t ff(uint32_t x, uint32_t y) { return x + y; }
 };
 
-// Engine variant ids (hs_set_config.variant): 0 Native, 1 Fast, then the
-// Mx masks that led the B200 sweep for 4-, 6- and 8-word nodes.
-constexpr int kNumVariants = 6;
-template <int ID> struct VariantOf;
+// Engine variant ids (hs_set_config.variant): 0 Native, 1 Fast, then one Mx
+// per mask of HS_MX_MASKS (hs_variants.h; set at build time).
+constexpr int kMxMasks[] = {HS_MX_MASKS};
+constexpr int kNumVariants = 2 + (int)(sizeof(kMxMasks) / sizeof(kMxMasks[0]));
+template <int ID> struct VariantOf { using T = Mx<kMxMasks[ID - 2]>; };
 template <> struct VariantOf<0> { using T = Native; };
 template <> struct VariantOf<1> { using T = Fast; };
-template <> struct VariantOf<2> { using T = Mx<248>; };
-template <> struct VariantOf<3> { using T = Mx<250>; };
-template <> struct VariantOf<4> { using T = Mx<104>; };
-template <> struct VariantOf<5> { using T = Mx<172>; };
 
 // Rounds [R0, R1) of SHA-256 on working state s, expanding the schedule in
 // place for rounds >= 16.  Fully unrolled so constant message words
@@ -365,6 +364,48 @@ __device__ __forceinline__ void chain_F(uint32_t* x, const uint32_t mid[8], cons
 #pragma unroll
       for (int j = 0; j < NW; j++) rec[(s + 1) * NW + j] = x[j];
     }
+  }
+}
+
+// Out-of-line form of chain_F for the leaf kernels.  Inlined into a large
+// kernel, the chain loop's register assignment (and with it the register-bank
+// conflicts that co-limit SHA-256 on sm_100a) depends on everything live
+// around it; compiled as its own function, the loop is allocated like the
+// standalone chain-step kernel the B200 sweep measured.  Arguments and result
+// travel by value so nothing spills to local memory.
+template <int NW>
+struct NodeW {
+  uint32_t w[NW];
+};
+struct State8 {
+  uint32_t w[8];
+};
+#ifndef HS_CHAIN_NOINLINE
+#define HS_CHAIN_NOINLINE 1
+#endif
+template <class V, int NW>
+__device__ __noinline__ NodeW<NW> chain_F_ool(NodeW<NW> x, State8 mid, Adrs a, uint32_t start, uint32_t steps,
+                                              uint32_t* rec) {
+  chain_F<V, NW>(x.w, mid.w, a, start, steps, rec);
+  return x;
+}
+// Measured on B200 (tools/variant_sweep.py, both builds): out of line is 3%
+// faster for 8-word nodes (256f TREE_Sign) and 2-7% slower for 4/6-word ones.
+template <class V, int NW>
+__device__ __forceinline__ void chain_F_leaf(uint32_t* x, const uint32_t mid[8], const Adrs& a, uint32_t start,
+                                             uint32_t steps, uint32_t* rec = nullptr) {
+  if constexpr (HS_CHAIN_NOINLINE && NW == 8) {
+    NodeW<NW> xv;
+    State8 m;
+#pragma unroll
+    for (int j = 0; j < NW; j++) xv.w[j] = x[j];
+#pragma unroll
+    for (int j = 0; j < 8; j++) m.w[j] = mid[j];
+    xv = chain_F_ool<V, NW>(xv, m, a, start, steps, rec);
+#pragma unroll
+    for (int j = 0; j < NW; j++) x[j] = xv.w[j];
+  } else {
+    chain_F<V, NW>(x, mid, a, start, steps, rec);
   }
 }
 

@@ -20,8 +20,11 @@ from .errors import HeroSignError, UsageError
 from .params import SET_INDEX, derive
 
 KERNELS = ("FORS_Sign", "TREE_Sign", "WOTS_Sign", "host")  # hs_set_config.variant order
-# SHA-256 arithmetic paths compiled into the library (csrc/sha256.cuh VariantOf<id>)
-VARIANTS = ("native", "fast", "mx248", "mx250", "mx104", "mx172")
+
+
+def variants() -> tuple[str, ...]:
+    """SHA-256 arithmetic paths compiled into the library, by variant id (csrc/hs_variants.h)."""
+    return _lib.variant_names()
 
 
 def _u8ptr(buf):
@@ -94,6 +97,7 @@ class Engine:
             "streams": c.streams,
             "shared_layers": c.shared_layers,
             "shared_auto": bool(c.shared_auto),
+            "fors_cta_levels": c.fors_cta_levels,
         }
 
     def set_config(self, set_id: str, **kw) -> dict:
@@ -113,6 +117,7 @@ class Engine:
         c.streams = int(cur["streams"])
         c.shared_layers = int(cur["shared_layers"])
         c.shared_auto = int(bool(cur["shared_auto"]))
+        c.fors_cta_levels = int(cur["fors_cta_levels"])
         self._check(_lib.lib().hs_config_set(self._h, SET_INDEX[set_id], ctypes.byref(c)), "hs_config_set")
         return self.config(set_id)
 

@@ -255,8 +255,9 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
     1. ``device_candidates`` enumerates every layout Algorithm 1 admits at
        S_max = opt-in smem (both Relax modes); each is timed (FORS_Sign kernel,
        CUDA events, serial mode), the ``top`` fastest are re-timed and the best
-       trimmed mean wins.
-    2. For each kernel every compiled SHA-256 path (engine.VARIANTS) is timed;
+       trimmed mean wins; then every split between in-CTA levels and the
+       batch-wide level grids (``fors_cta_levels``) is timed for it.
+    2. For each kernel every compiled SHA-256 path (engine.variants()) is timed;
        the fastest replaces 'native' only if it is faster by more than
        ``tie_tolerance`` (the reference's rule, tuner.py:206-218).
     Returns the chosen config plus the timing table; the engine is left
@@ -286,22 +287,32 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
     best = min(table, key=lambda r: r["fors_ms"])
     engine.set_config(set_id, fors_trees_per_set=best["trees_per_set"], fors_sets_fused=best["sets_fused"],
                       fors_relax=best["relax"])
+    # 1b. split between the CTA's in-shared-memory levels and the batch-wide
+    #     level grids for the chosen layout (fors_cta_levels; -1 = auto)
+    ltable = {}
+    for lc in [-1] + list(range(1 if best["relax"] else 0, p.log_t + 1)):
+        engine.set_config(set_id, fors_cta_levels=lc)
+        ltable[lc] = _trimmed_mean(_kernel_ms(engine, set_id, count, "FORS_Sign", reps))
+    best_lc = min(ltable, key=ltable.get)
+    engine.set_config(set_id, fors_cta_levels=best_lc)
+    best = dict(best, fors_cta_levels=best_lc, fors_ms=ltable[best_lc])
     variants = dict(base["variant"])
     vtable = {}
     if tune_variants:
-        from .engine import VARIANTS
+        from .engine import variants as compiled_paths
 
+        names = compiled_paths()
         for kernel in ("FORS_Sign", "TREE_Sign", "WOTS_Sign"):
             cell = {}
-            for v, name in enumerate(VARIANTS):
+            for v, name in enumerate(names):
                 var = dict(variants)
                 var[kernel] = v
                 engine.set_config(set_id, variant=var)
                 cell[name] = _trimmed_mean(_kernel_ms(engine, set_id, count, kernel, reps))
             # a non-native path replaces native only when faster by more than
             # tie_tolerance (the reference's rule, tuner.py:206-218)
-            best_v = min(range(len(VARIANTS)), key=lambda v: cell[VARIANTS[v]])
-            variants[kernel] = best_v if cell[VARIANTS[best_v]] < cell["native"] * (1.0 - tie_tolerance) else 0
+            best_v = min(range(len(names)), key=lambda v: cell[names[v]])
+            variants[kernel] = best_v if cell[names[best_v]] < cell["native"] * (1.0 - tie_tolerance) else 0
             vtable[kernel] = cell
         engine.set_config(set_id, variant=variants)
     # 3. multi-stream batching: T prioritised sub-batches per graph, timed end to
@@ -331,5 +342,6 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
     best_T = min(stable, key=stable.get)
     engine.set_config(set_id, streams=best_T)
     return {"set": set_id, "count": count, "smem_optin": info["smem_optin"], "layouts": table,
-            "best_layout": best, "variants": variants, "variant_ms": vtable, "streams_ms": stable,
+            "best_layout": best, "cta_levels_ms": ltable, "variants": variants, "variant_ms": vtable,
+            "streams_ms": stable,
             "config": engine.config(set_id)}

@@ -11,7 +11,7 @@ import pytest
 from conftest import GOLDEN_DIR, SETS
 
 import paper_2512_23969_b200 as hs
-from paper_2512_23969_b200.engine import VARIANTS
+from paper_2512_23969_b200.engine import variants
 from paper_2512_23969_b200.params import derive
 
 pytestmark = pytest.mark.gpu
@@ -79,7 +79,7 @@ def test_mixed_batch_vs_oracle(eng, oracle_mod, set_id):
 
 
 @pytest.mark.parametrize("set_id", SETS)
-@pytest.mark.parametrize("variant", range(len(VARIANTS)))
+@pytest.mark.parametrize("variant", range(len(variants())))
 @pytest.mark.parametrize("stash", [True, False])
 def test_layouts_and_variants(eng, oracle_mod, set_id, variant, stash):
     """Every FORS fusion layout / relax mode and every compiled SHA-256 path give identical bytes."""
@@ -100,6 +100,29 @@ def test_layouts_and_variants(eng, oracle_mod, set_id, variant, stash):
                            variant={k: variant for k in ("FORS_Sign", "TREE_Sign", "WOTS_Sign", "host")})
             assert eng.sign_batch(set_id, msgs) == ref, (nt, f, rx)
         assert eng.keygen_batch(set_id, [seed])[0] == sk  # keygen root kernel on this path
+    finally:
+        eng.set_config(set_id, **base)
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_fors_upper_levels_split(eng, oracle_mod, set_id):
+    """Any split between in-CTA FORS levels and the batch-wide level grids
+    (fors_cta_levels -1 = auto, 0..log_t) gives identical bytes, with and
+    without Relax and with uneven passes (vexec.py:437-463 semantics)."""
+    p = derive(set_id)
+    rng = random.Random(1234)
+    sk = oracle_mod.keygen(set_id, rng.randbytes(3 * p.n))
+    msgs = [rng.randbytes(rng.choice([0, 32, 77])) for _ in range(5)]
+    ref = [oracle_mod.sign(set_id, sk, m) for m in msgs]
+    eng.upload_keys(set_id, sk)
+    base = eng.config(set_id)
+    try:
+        for nt, f, rx in ((1, 1, 0), (1, 3, 0), (1, 2, 1), (base["fors_trees_per_set"], base["fors_sets_fused"],
+                                                           int(base["fors_relax"]))):
+            for lc in sorted({-1, 0, 1, 2, p.log_t - 1, p.log_t}):
+                eng.set_config(set_id, fors_trees_per_set=nt, fors_sets_fused=f, fors_relax=bool(rx),
+                               fors_cta_levels=lc)
+                assert eng.sign_batch(set_id, msgs) == ref, (nt, f, rx, lc)
     finally:
         eng.set_config(set_id, **base)
 

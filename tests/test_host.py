@@ -3,6 +3,7 @@
 from __future__ import annotations
 
 import ctypes
+import os
 import re
 from pathlib import Path
 
@@ -131,3 +132,15 @@ def test_cli_usage_errors(tmp_path):
     assert cli.main(["verify", "128f", "--pk", str(tmp_path / "pk"), "--message", str(tmp_path / "m"),
                      "--sig", str(tmp_path / "s")]) == cli.EXIT_VERIFY_FAIL
     assert cli.main(["frobnicate"]) == 2
+
+
+def test_compiled_sha_paths(L):
+    """hs_variants reports native, fast and the Mx<mask> paths listed in hs_variants.h."""
+    names = _lib.variant_names()
+    assert names[:2] == ("native", "fast")
+    hdr = (ROOT / "paper_2512_23969_b200" / "csrc" / "hs_variants.h").read_text()
+    default = re.search(r"#define HS_MX_MASKS ([\d, ]+)", hdr).group(1)
+    masks = [int(x) for x in default.split(",")]
+    if not os.environ.get("HERO_SIGN_LIB"):
+        assert names[2:] == tuple(f"mx{m}" for m in masks)
+    assert all(0 <= int(n[2:]) < 256 for n in names[2:])

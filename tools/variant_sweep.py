@@ -1,5 +1,5 @@
 """Time FORS_Sign / TREE_Sign / WOTS_Sign under every compiled SHA-256 path
-(engine.VARIANTS) for each parameter set, with the set's current layout.
+(engine.variants(); HERO_SIGN_LIB selects a sweep build) for each parameter set, with the set's current layout.
 
     python tools/variant_sweep.py [--count 4096] [--reps 5]
 """
@@ -14,7 +14,7 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 import paper_2512_23969_b200 as hs  # noqa: E402
-from paper_2512_23969_b200.engine import VARIANTS  # noqa: E402
+from paper_2512_23969_b200.engine import variants  # noqa: E402
 from paper_2512_23969_b200.tuner import _kernel_ms, _synthetic, _trimmed_mean  # noqa: E402
 
 
@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--sets", default="128f,192f,256f")
     a = ap.parse_args()
     eng = hs.get_engine(0)
+    names = variants()
     out = {}
     for set_id in a.sets.split(","):
         _synthetic(eng, set_id, a.count)
@@ -32,7 +33,7 @@ def main():
         res = {}
         try:
             for kernel in ("TREE_Sign", "FORS_Sign"):
-                for v, name in enumerate(VARIANTS):
+                for v, name in enumerate(names):
                     var = dict(base["variant"])
                     var[kernel] = v
                     eng.set_config(set_id, variant=var, wots_from_tree=True)
