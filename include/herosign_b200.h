@@ -86,6 +86,10 @@ typedef struct {
                                  whole tree in the CTA (reference shape,
                                  vexec.py:437-463), -1 = auto (leaves only:
                                  the measured best on B200)                  */
+  int32_t tree_split;         /* 1: TREE_Sign as two grids -- one thread per
+                                 WOTS chain, then one per leaf (T_len +
+                                 Merkle); 0: one thread per leaf runs its
+                                 chains and T_len (fused)                    */
 } hs_set_config;
 
 HS_API int hs_open(int device, hs_t **out);

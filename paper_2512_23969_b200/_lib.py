@@ -49,6 +49,7 @@ class SetConfig(ctypes.Structure):
         ("shared_layers", ctypes.c_int32),
         ("shared_auto", ctypes.c_int32),
         ("fors_cta_levels", ctypes.c_int32),
+        ("tree_split", ctypes.c_int32),
     ]
 
 

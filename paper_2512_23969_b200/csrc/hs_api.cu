@@ -104,6 +104,7 @@ hs_set_config default_config(int set) {
   c.shared_layers = shared_max(set);
   c.shared_auto = 1;
   c.fors_cta_levels = -1;
+  c.tree_split = 1;
   return c;
 }
 
@@ -143,6 +144,7 @@ struct Buffers {
   uint32_t* shared = nullptr; size_t shared_cap = 0;   // subtree-sharing table
   uint8_t* key_used = nullptr; size_t key_used_cap = 0;
   uint32_t* fnodes[2] = {nullptr, nullptr}; size_t fnodes_cap[2] = {0, 0};  // upper FORS levels
+  uint32_t* ends = nullptr; size_t ends_cap = 0;  // split TREE_Sign chain ends
   // pinned staging
   uint8_t* h_msgs = nullptr; size_t h_msgs_cap = 0;
   uint64_t* h_offs = nullptr; size_t h_offs_cap = 0;
@@ -253,6 +255,7 @@ int check_layout(hs_t* h, int set, const hs_set_config& c) {
   if (c.shared_layers < 0 || c.shared_layers > shared_max(set))
     return fail(h, HS_E_CONFIG, "shared_layers must be in 0..%d for this set", shared_max(set));
   if (c.shared_auto != 0 && c.shared_auto != 1) return fail(h, HS_E_CONFIG, "shared_auto must be 0 or 1");
+  if (c.tree_split != 0 && c.tree_split != 1) return fail(h, HS_E_CONFIG, "tree_split must be 0 or 1");
   if (c.fors_cta_levels < -1 || c.fors_cta_levels > I.log_t)
     return fail(h, HS_E_CONFIG, "fors_cta_levels must be -1 (auto) or in 0..%d", I.log_t);
   return HS_OK;
@@ -299,6 +302,12 @@ size_t fors_node_words(int set, const hs_set_config& c, uint32_t count, int b) {
   return L >= I.log_t ? 0 : (size_t)count * I.k * ((size_t)I.t >> (L + b)) * (I.n / 4);
 }
 
+// words of the split TREE_Sign's chain-end buffer for `count` messages
+size_t chain_end_words(int set, uint32_t count) {
+  const SetInfo& I = kInfo[set];
+  return (size_t)count * I.d * I.leaves * I.wots_len * (I.n / 4);
+}
+
 // Arguments for messages [first, first + count) of the staged batch.  Message
 // offsets stay absolute into the staged blob; every per-message buffer is
 // offset by `first`, so sub-batches are independent launches.
@@ -339,7 +348,20 @@ LaunchArgs make_args(hs_t* h, int set, uint32_t first, uint32_t count) {
     a.shared_layers = L;
     a.key_used = B.key_used;
   }
+  if (St.cfg.tree_split && B.ends && B.ends_cap >= chain_end_words(set, first + count))
+    a.chain_ends = B.ends + (size_t)first * (I.d - a.shared_layers) * I.leaves * I.wots_len * (I.n / 4);
   return a;
+}
+
+// TREE_Sign on one stream: split (chain grid, then leaf / Merkle grid) or fused.
+cudaError_t enqueue_tree(int set, const hs_set_config& c, const LaunchArgs& a, cudaStream_t s, int& kernels) {
+  if (!a.chain_ends) {
+    kernels++;
+    return launch(set, K_TREE, c.variant[1], a, s);
+  }
+  kernels += 2;
+  cudaError_t e = launch(set, K_TREE_CHAIN, c.variant[1], a, s);
+  return e == cudaSuccess ? launch(set, K_TREE_ROOT, c.variant[1], a, s) : e;
 }
 
 // FORS_Sign, the batch-wide upper FORS levels (if any) and T_k on one stream.
@@ -357,14 +379,16 @@ cudaError_t enqueue_fors(int set, const hs_set_config& c, const LaunchArgs& a, c
   return e;
 }
 
-// Upper-level FORS buffers for `count` messages under the current config.
+// Config-dependent scratch for `count` messages: upper FORS levels and the
+// split TREE_Sign's chain ends.
 int ensure_fors_nodes(hs_t* h, int set, uint32_t count) {
   Buffers& B = h->buf[set];
-  if (fors_node_words(set, h->sets[set].cfg, count, 0) == 0) return HS_OK;
-  void* before[2] = {B.fnodes[0], B.fnodes[1]};
-  for (int b = 0; b < 2; b++)
-    CUDA_TRY(h, grow(B.fnodes[b], B.fnodes_cap[b], fors_node_words(set, h->sets[set].cfg, count, b)));
-  void* after[2] = {B.fnodes[0], B.fnodes[1]};
+  const hs_set_config& c = h->sets[set].cfg;
+  void* before[3] = {B.fnodes[0], B.fnodes[1], B.ends};
+  if (fors_node_words(set, c, count, 0) != 0)
+    for (int b = 0; b < 2; b++) CUDA_TRY(h, grow(B.fnodes[b], B.fnodes_cap[b], fors_node_words(set, c, count, b)));
+  if (c.tree_split) CUDA_TRY(h, grow(B.ends, B.ends_cap, chain_end_words(set, count)));
+  void* after[3] = {B.fnodes[0], B.fnodes[1], B.ends};
   if (std::memcmp(before, after, sizeof before) != 0) {
     B.gen++;
     drop_graphs(h);
@@ -381,7 +405,7 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
   };
   cudaError_t e;
 #define TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
-  int kernels = 3 + (a.shared_layers > 0 ? 1 : 0);  // + the FORS branch, counted by enqueue_fors
+  int kernels = 2 + (a.shared_layers > 0 ? 1 : 0);  // + the FORS / TREE branches, counted by enqueue_*
   TRY(rec(0, h->s0));
   if (a.shared_layers > 0) TRY(cudaMemsetAsync(a.key_used, 0, a.nkeys, h->s0));
   TRY(launch(set, K_PREP, c.variant[3], a, h->s0));
@@ -389,7 +413,7 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
   if (serial) {
     TRY(enqueue_fors(set, c, a, h->s0, kernels));
     TRY(rec(2, h->s0));
-    TRY(launch(set, K_TREE, c.variant[1], a, h->s0));
+    TRY(enqueue_tree(set, c, a, h->s0, kernels));
     TRY(rec(3, h->s0));  // [2,3] = per-message TREE_Sign only (the roofline kernel)
     if (a.shared_layers > 0) TRY(launch(set, K_TREE_SHARED, c.variant[1], a, h->s0));
     TRY(rec(5, h->s0));
@@ -405,7 +429,7 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
     TRY(enqueue_fors(set, c, a, h->s1, kernels));
     TRY(rec(2, h->s1));
     TRY(cudaEventRecord(h->join, h->s1));
-    TRY(launch(set, K_TREE, c.variant[1], a, h->s0));
+    TRY(enqueue_tree(set, c, a, h->s0, kernels));
     TRY(rec(3, h->s0));
     TRY(cudaStreamWaitEvent(h->s0, h->join, 0));
     TRY(rec(5, h->s0));
@@ -464,13 +488,13 @@ cudaError_t enqueue_batch(hs_t* h, int set, uint32_t count, int T, bool capture)
     cudaStream_t q = h->q[1 + 2 * j], qf = h->q[2 + 2 * j];
     TRY(cudaStreamWaitEvent(q, h->fork, 0));
     TRY(cudaStreamWaitEvent(qf, h->fork, 0));
-    TRY(launch(set, K_TREE, c.variant[1], a, q));
+    TRY(enqueue_tree(set, c, a, q, kernels));
     TRY(enqueue_fors(set, c, a, qf, kernels));
     TRY(cudaEventRecord(h->fjoin[j], qf));
     TRY(cudaStreamWaitEvent(q, h->fjoin[j], 0));
     if (all.shared_layers > 0) TRY(cudaStreamWaitEvent(q, h->sh_done, 0));
     TRY(launch(set, a.stash ? K_WOTS_GATHER : K_WOTS, c.variant[2], a, q));
-    kernels += 2;
+    kernels += 1;
     TRY(rec(h->done[j], q));
     TRY(cudaEventRecord(h->joins[j], q));
     TRY(cudaStreamWaitEvent(h->s0, h->joins[j], 0));
@@ -679,6 +703,7 @@ void hs_close(hs_t* h) {
     cudaFree(B.key_used);
     cudaFree(B.fnodes[0]);
     cudaFree(B.fnodes[1]);
+    cudaFree(B.ends);
     cudaFree(h->sets[s].sk_raw);
   }
   if (h->flush) cudaFree(h->flush);

@@ -24,6 +24,8 @@ enum KernelId : int {
   K_WOTS_GATHER = 8,
   K_TREE_SHARED = 9,
   K_FORS_LEVEL = 10,
+  K_TREE_CHAIN = 11,
+  K_TREE_ROOT = 12,
 };
 
 // variant: SHA-256 arithmetic path id, 0..kNumVariants-1 (sha256.cuh VariantOf)

@@ -78,6 +78,11 @@ struct LaunchArgs {
   int fors_cta_levels;
   int fors_level;            // level computed by one fors_level_kernel launch
   uint32_t* fors_nodes[2];
+  // Split TREE_Sign: tree_chain_kernel writes every chain end of the batch's
+  // per-message leaves here ([msg][layer][leaf][chain][NW]); tree_root_kernel
+  // compresses them into leaves and reduces the subtrees.  nullptr = fused
+  // tree_sign_kernel (thread = leaf runs its own chains).
+  uint32_t* chain_ends;
 };
 
 __device__ __forceinline__ uint64_t shr64(uint64_t x, int s) { return s >= 64 ? 0ull : (x >> s); }
@@ -277,11 +282,16 @@ constexpr int kLeafColumnWords = 40;  // per-thread smem column: 32-word T_len r
 #ifndef HS_TREE_MIN_BLOCKS
 #define HS_TREE_MIN_BLOCKS 5
 #endif
-// 5 blocks -> <= 96 registers, 20 warps / SM; 256f (8-word nodes) uses 4 blocks / 128 registers
+#ifndef HS_TREE_MIN_BLOCKS_8W
+#define HS_TREE_MIN_BLOCKS_8W 3
+#endif
+// 5 blocks -> <= 96 registers, 20 warps / SM; 256f (8-word nodes) uses 3 blocks / 168 registers
+// (B200 sweep over 3..6 blocks x SHA paths, profiles/r01_tree_occupancy.txt)
 constexpr int kTreeMinBlocks = HS_TREE_MIN_BLOCKS;
+constexpr int kTreeMinBlocks8 = HS_TREE_MIN_BLOCKS_8W;
 
 template <int S, class V>
-__global__ void __launch_bounds__(kTreeBlock, (S == 2 ? 4 : kTreeMinBlocks)) tree_sign_kernel(LaunchArgs a) {
+__global__ void __launch_bounds__(kTreeBlock, (S == 2 ? kTreeMinBlocks8 : kTreeMinBlocks)) tree_sign_kernel(LaunchArgs a) {
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
   __shared__ uint32_t tbuf[kLeafColumnWords * kTreeBlock];
@@ -306,6 +316,138 @@ __global__ void __launch_bounds__(kTreeBlock, (S == 2 ? 4 : kTreeMinBlocks)) tre
                         ? a.stash + ((size_t)msg * Pr::d + layer) * Pr::wots_len * Pr::w * NW
                         : nullptr;
     wots_leaf<S, V>(*K, layer, tree, leaf, &tbuf[threadIdx.x], kTreeBlock, node, rec);
+  }
+  uint8_t* auth = a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_ht + (size_t)layer * Pr::layer_bytes +
+                  Pr::wots_sig_bytes;
+#pragma unroll 1
+  for (int lvl = 1; lvl <= Pr::hp; lvl++) {
+    const uint32_t below = leaf >> (lvl - 1);
+    const bool holder_below = (leaf & ((1u << (lvl - 1)) - 1u)) == 0u;
+    if (valid && holder_below && below == ((leaf_idx >> (lvl - 1)) ^ 1u))
+      store_node<NW>(auth + (lvl - 1) * Pr::n, node);
+    uint32_t other[NW];
+#pragma unroll
+    for (int j = 0; j < NW; j++) other[j] = __shfl_down_sync(0xffffffffu, node[j], 1u << (lvl - 1));
+    if (valid && (leaf & ((1u << lvl) - 1u)) == 0u) {
+      uint32_t m[2 * NW];
+#pragma unroll
+      for (int j = 0; j < NW; j++) { m[j] = node[j]; m[NW + j] = other[j]; }
+      uint32_t mid[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) mid[j] = K->thash_mid[j];
+      thash_reg<V, 2 * NW>(node, mid, make_adrs(layer, tree, ADDR_HASHTREE, 0, (uint32_t)lvl, leaf >> lvl), m);
+    }
+  }
+  if (valid && leaf == 0) {
+    uint32_t* r = a.roots + ((size_t)msg * (Pr::d + 1) + layer + 1) * 8;
+#pragma unroll
+    for (int j = 0; j < NW; j++) r[j] = node[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Split TREE_Sign.  Part 1, tree_chain_kernel: thread = (message, layer, leaf,
+// chain) runs PRF + (w-1) F for one WOTS chain (wots.py:42-65) and writes the
+// chain end; the signing leaf's chains also record every position for the
+// WOTS gather.  A thread holds one chain state, so the kernel keeps the
+// register budget of the standalone chain step (the B200 sweep's shape,
+// tools/sha_sweep) instead of the fused leaf kernel's 96, and the grid has
+// wots_len times more threads.  Part 2, tree_root_kernel: thread = (message,
+// layer, leaf) compresses its wots_len chain ends into the leaf (T_len,
+// wots.py:140-143, streamed straight from global memory) and the leaves of a
+// subtree are reduced with warp shuffles as in tree_sign_kernel.
+// ---------------------------------------------------------------------------
+constexpr int kChainBlock = 128;
+
+template <int S, class V>
+__global__ void __launch_bounds__(kChainBlock) tree_chain_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  constexpr int NW = Pr::NW;
+  const uint32_t dl = (uint32_t)(Pr::d - a.shared_layers);
+  const uint64_t gid = (uint64_t)blockIdx.x * kChainBlock + threadIdx.x;
+  if (gid >= (uint64_t)a.count * dl * Pr::leaves * Pr::wots_len) return;
+  const uint32_t chain = (uint32_t)(gid % Pr::wots_len);
+  const uint64_t lid = gid / Pr::wots_len;             // (msg, layer, leaf)
+  const uint32_t leaf = (uint32_t)(lid % Pr::leaves);
+  const uint32_t layer = (uint32_t)((lid / Pr::leaves) % dl);
+  const uint32_t msg = (uint32_t)(lid / ((uint64_t)Pr::leaves * dl));
+  const MsgPlan pl = a.plans[msg];
+  const KeyDev& K = a.keys[pl.key];
+  uint64_t tree;
+  uint32_t leaf_idx;
+  layer_coords<S>(pl, (int)layer, tree, leaf_idx);
+  uint32_t mid[8], sks[NW], st[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) mid[j] = K.thash_mid[j];
+#pragma unroll
+  for (int j = 0; j < NW; j++) sks[j] = K.sk_seed[j];
+  const Adrs wa = make_adrs(layer, tree, ADDR_WOTS, leaf, chain, 0);
+  prf_reg<V, NW>(st, sks, wa);                          // chain secret (wots.py:63-65)
+  uint32_t x[NW];
+#pragma unroll
+  for (int j = 0; j < NW; j++) x[j] = st[j];
+  uint32_t* rec = (a.stash && leaf == leaf_idx)
+                      ? a.stash + (((size_t)msg * Pr::d + layer) * Pr::wots_len + chain) * Pr::w * NW
+                      : nullptr;
+  if (rec) {
+#pragma unroll
+    for (int j = 0; j < NW; j++) rec[j] = x[j];
+  }
+  chain_F<V, NW>(x, mid, wa, 0u, (uint32_t)(Pr::w - 1), rec);
+  uint32_t* e = a.chain_ends + gid * NW;
+#pragma unroll
+  for (int j = 0; j < NW; j++) e[j] = x[j];
+}
+
+// Word k (0-based, after the PK.seed midstate block) of the T_len input
+// ADRS(22 B) || ends (M = wots_len * NW words) || SHA-256 padding, with the
+// chain ends read from global memory (thash_reg's layout, hashes.py:124-137).
+template <int M>
+__device__ __forceinline__ uint32_t tlen_word(uint32_t k, const uint32_t aw[6], const uint32_t* e, uint32_t len_bits,
+                                              uint32_t last) {
+  if (k < 5) return k == 0 ? aw[0] : k == 1 ? aw[1] : k == 2 ? aw[2] : k == 3 ? aw[3] : aw[4];  // no local array
+  if (k == 5) return join16(aw[5], e[0]);
+  if (k < 5 + M) return join16(e[k - 6], e[k - 5]);
+  if (k == 5 + M) return (e[M - 1] << 16) | 0x8000u;
+  return k == last ? len_bits : 0u;
+}
+
+template <int S, class V>
+__global__ void __launch_bounds__(kTreeBlock) tree_root_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  constexpr int NW = Pr::NW;
+  constexpr int M = Pr::wots_len * NW;
+  constexpr uint32_t total = 22u + (uint32_t)(Pr::wots_len * Pr::n);  // bytes after the midstate block
+  constexpr uint32_t nblk = (total + 9u + 63u) / 64u;
+  const uint32_t dl = (uint32_t)(Pr::d - a.shared_layers);
+  const uint64_t per_msg = (uint64_t)dl * Pr::leaves;
+  const uint64_t gid = (uint64_t)blockIdx.x * kTreeBlock + threadIdx.x;
+  const bool valid = gid < (uint64_t)a.count * per_msg;
+  const uint32_t msg = valid ? (uint32_t)(gid / per_msg) : 0u;
+  const uint32_t rem = (uint32_t)(gid % per_msg);
+  const uint32_t layer = rem / Pr::leaves;
+  const uint32_t leaf = rem % Pr::leaves;
+
+  uint32_t node[8];
+  uint64_t tree = 0;
+  uint32_t leaf_idx = 0;
+  const KeyDev* K = nullptr;
+  if (valid) {
+    const MsgPlan pl = a.plans[msg];
+    K = &a.keys[pl.key];
+    layer_coords<S>(pl, (int)layer, tree, leaf_idx);
+    const Adrs pa = make_adrs(layer, tree, ADDR_WOTS_PK, leaf, 0, 0);
+    const uint32_t aw[6] = {pa.w0, pa.w1, pa.w2, pa.w3, pa.w4, pa.h5};
+    const uint32_t* e = a.chain_ends + gid * M;
+#pragma unroll
+    for (int j = 0; j < 8; j++) node[j] = K->thash_mid[j];
+#pragma unroll 1
+    for (uint32_t b = 0; b < nblk; b++) {
+      uint32_t W[16];
+#pragma unroll
+      for (int j = 0; j < 16; j++) W[j] = tlen_word<M>(16u * b + j, aw, e, (64u + total) * 8u, 16u * nblk - 1u);
+      compress<V>(node, W);
+    }
   }
   uint8_t* auth = a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_ht + (size_t)layer * Pr::layer_bytes +
                   Pr::wots_sig_bytes;
@@ -368,7 +510,7 @@ struct Shared {
 };
 
 template <int S, class V>
-__global__ void __launch_bounds__(kTreeBlock, (S == 2 ? 4 : kTreeMinBlocks)) tree_shared_kernel(LaunchArgs a) {
+__global__ void __launch_bounds__(kTreeBlock, (S == 2 ? kTreeMinBlocks8 : kTreeMinBlocks)) tree_shared_kernel(LaunchArgs a) {
   using Pr = P<S>;
   using Sh = Shared<S>;
   constexpr int NW = Pr::NW;

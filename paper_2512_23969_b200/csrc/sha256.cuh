@@ -381,7 +381,7 @@ struct State8 {
   uint32_t w[8];
 };
 #ifndef HS_CHAIN_NOINLINE
-#define HS_CHAIN_NOINLINE 1
+#define HS_CHAIN_NOINLINE 0
 #endif
 template <class V, int NW>
 __device__ __noinline__ NodeW<NW> chain_F_ool(NodeW<NW> x, State8 mid, Adrs a, uint32_t start, uint32_t steps,
@@ -389,8 +389,10 @@ __device__ __noinline__ NodeW<NW> chain_F_ool(NodeW<NW> x, State8 mid, Adrs a, u
   chain_F<V, NW>(x.w, mid.w, a, start, steps, rec);
   return x;
 }
-// Measured on B200 (tools/variant_sweep.py, both builds): out of line is 3%
-// faster for 8-word nodes (256f TREE_Sign) and 2-7% slower for 4/6-word ones.
+// Measured on B200 (tools/variant_sweep.py): out of line was 3% faster for
+// 8-word nodes at 4 blocks/SM but 2-7% slower for 4/6-word nodes, and inline
+// wins again at the 3 blocks/SM the fused 256f kernel now uses; kept as a
+// build option (HS_CHAIN_NOINLINE=1) for the next sweep.
 template <class V, int NW>
 __device__ __forceinline__ void chain_F_leaf(uint32_t* x, const uint32_t mid[8], const Adrs& a, uint32_t start,
                                              uint32_t steps, uint32_t* rec = nullptr) {

@@ -98,6 +98,7 @@ class Engine:
             "shared_layers": c.shared_layers,
             "shared_auto": bool(c.shared_auto),
             "fors_cta_levels": c.fors_cta_levels,
+            "tree_split": bool(c.tree_split),
         }
 
     def set_config(self, set_id: str, **kw) -> dict:
@@ -118,6 +119,7 @@ class Engine:
         c.shared_layers = int(cur["shared_layers"])
         c.shared_auto = int(bool(cur["shared_auto"]))
         c.fors_cta_levels = int(cur["fors_cta_levels"])
+        c.tree_split = int(bool(cur["tree_split"]))
         self._check(_lib.lib().hs_config_set(self._h, SET_INDEX[set_id], ctypes.byref(c)), "hs_config_set")
         return self.config(set_id)
 

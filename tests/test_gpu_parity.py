@@ -82,7 +82,8 @@ def test_mixed_batch_vs_oracle(eng, oracle_mod, set_id):
 @pytest.mark.parametrize("variant", range(len(variants())))
 @pytest.mark.parametrize("stash", [True, False])
 def test_layouts_and_variants(eng, oracle_mod, set_id, variant, stash):
-    """Every FORS fusion layout / relax mode and every compiled SHA-256 path give identical bytes."""
+    """Every FORS fusion layout / relax mode, every compiled SHA-256 path and both
+    TREE_Sign shapes (split / fused) give identical bytes."""
     p = derive(set_id)
     rng = random.Random(99)
     seed = rng.randbytes(3 * p.n)
@@ -95,10 +96,12 @@ def test_layouts_and_variants(eng, oracle_mod, set_id, variant, stash):
                "192f": [(1, 1, 0), (3, 3, 0), (4, 2, 1), (2, 5, 1)],
                "256f": [(1, 1, 0), (2, 2, 1), (1, 5, 1), (3, 6, 1)]}[set_id]
     try:
-        for nt, f, rx in layouts:
+        for i, (nt, f, rx) in enumerate(layouts):
+            # alternate the split (chain grid + leaf grid) and fused TREE_Sign
             eng.set_config(set_id, fors_trees_per_set=nt, fors_sets_fused=f, fors_relax=bool(rx), wots_from_tree=stash,
-                           variant={k: variant for k in ("FORS_Sign", "TREE_Sign", "WOTS_Sign", "host")})
-            assert eng.sign_batch(set_id, msgs) == ref, (nt, f, rx)
+                           variant={k: variant for k in ("FORS_Sign", "TREE_Sign", "WOTS_Sign", "host")},
+                           tree_split=(i % 2 == 0))
+            assert eng.sign_batch(set_id, msgs) == ref, (nt, f, rx, i % 2 == 0)
         assert eng.keygen_batch(set_id, [seed])[0] == sk  # keygen root kernel on this path
     finally:
         eng.set_config(set_id, **base)

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--count", type=int, default=4096)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--sets", default="128f,192f,256f")
+    ap.add_argument("--kernels", default="TREE_Sign,FORS_Sign")
+    ap.add_argument("--tree-split", default="1", help="comma list of tree_split values to time TREE_Sign under")
     a = ap.parse_args()
     eng = hs.get_engine(0)
     names = variants()
@@ -32,13 +34,16 @@ def main():
         base = eng.config(set_id)
         res = {}
         try:
-            for kernel in ("TREE_Sign", "FORS_Sign"):
-                for v, name in enumerate(names):
-                    var = dict(base["variant"])
-                    var[kernel] = v
-                    eng.set_config(set_id, variant=var, wots_from_tree=True)
-                    res.setdefault(kernel, {})[name] = round(_trimmed_mean(_kernel_ms(eng, set_id, a.count, kernel,
-                                                                                      a.reps)), 4)
+            for kernel in a.kernels.split(","):
+                splits = [int(x) for x in a.tree_split.split(",")] if kernel == "TREE_Sign" else [1]
+                for ts in splits:
+                    key = f"{kernel}/split{ts}" if kernel == "TREE_Sign" else kernel
+                    for v, name in enumerate(names):
+                        var = dict(base["variant"])
+                        var[kernel] = v
+                        eng.set_config(set_id, variant=var, wots_from_tree=True, tree_split=bool(ts))
+                        res.setdefault(key, {})[name] = round(
+                            _trimmed_mean(_kernel_ms(eng, set_id, a.count, kernel, a.reps)), 4)
         finally:
             eng.set_config(set_id, **base)
         out[set_id] = res
