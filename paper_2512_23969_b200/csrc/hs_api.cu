@@ -221,11 +221,15 @@ int fail(hs_t* h, int code, const char* fmt, ...) {
 
 bool valid_set(int set) { return set >= 0 && set <= 2; }
 
+// Every field of the set's config (all int32): a captured graph is reused only
+// for an identical config.
 std::string cfg_fingerprint(const hs_set_config& c) {
-  char b[160];
-  snprintf(b, sizeof b, "%d/%d/%d/%d%d%d%d/%d/%d/%d", c.fors_trees_per_set, c.fors_sets_fused, c.fors_relax,
-           c.variant[0], c.variant[1], c.variant[2], c.variant[3], c.wots_from_tree, c.shared_layers, c.shared_auto);
-  return b;
+  static_assert(sizeof(hs_set_config) % sizeof(int32_t) == 0, "hs_set_config must be all int32 fields");
+  int32_t f[sizeof(hs_set_config) / sizeof(int32_t)];
+  std::memcpy(f, &c, sizeof f);
+  std::string out;
+  for (int32_t v : f) out += std::to_string(v) + "/";
+  return out;
 }
 
 void drop_graphs(hs_t* h) {

@@ -130,6 +130,31 @@ def test_fors_upper_levels_split(eng, oracle_mod, set_id):
         eng.set_config(set_id, **base)
 
 
+def test_config_change_rebuilds_graph(eng, oracle_mod):
+    """A captured batch graph is reused only for an identical config: toggling
+    tree_split / fors_cta_levels on the same layout changes the kernels run."""
+    set_id = "128f"
+    p = derive(set_id)
+    rng = random.Random(77)
+    sk = oracle_mod.keygen(set_id, rng.randbytes(3 * p.n))
+    msgs = [rng.randbytes(32) for _ in range(3)]
+    ref = [oracle_mod.sign(set_id, sk, m) for m in msgs]
+    eng.upload_keys(set_id, sk)
+    base = eng.config(set_id)
+    try:
+        counts = {}
+        for split, lc in ((True, -1), (False, p.log_t), (True, -1)):
+            eng.set_config(set_id, tree_split=split, fors_cta_levels=lc, streams=1, shared_layers=0)
+            n0 = eng.launch_count
+            assert eng.sign_batch(set_id, msgs) == ref, (split, lc)
+            counts.setdefault((split, lc), []).append(eng.launch_count - n0)
+        # split TREE_Sign adds the leaf grid; leaves-only FORS adds log_t level grids
+        assert counts[(True, -1)][0] - counts[(False, p.log_t)][0] == 1 + p.log_t
+        assert counts[(True, -1)][0] == counts[(True, -1)][1]
+    finally:
+        eng.set_config(set_id, **base)
+
+
 @pytest.mark.parametrize("set_id", SETS)
 def test_verify_gpu(eng, golden, set_id):
     p = derive(set_id)
