@@ -357,10 +357,16 @@ __global__ void __launch_bounds__(kTreeBlock, (S == 2 ? kTreeMinBlocks8 : kTreeM
 // wots.py:140-143, streamed straight from global memory) and the leaves of a
 // subtree are reduced with warp shuffles as in tree_sign_kernel.
 // ---------------------------------------------------------------------------
-constexpr int kChainBlock = 128;
+#ifndef HS_CHAIN_BLOCK
+#define HS_CHAIN_BLOCK 128
+#endif
+#ifndef HS_CHAIN_MIN_BLOCKS
+#define HS_CHAIN_MIN_BLOCKS 1
+#endif
+constexpr int kChainBlock = HS_CHAIN_BLOCK;
 
 template <int S, class V>
-__global__ void __launch_bounds__(kChainBlock) tree_chain_kernel(LaunchArgs a) {
+__global__ void __launch_bounds__(kChainBlock, HS_CHAIN_MIN_BLOCKS) tree_chain_kernel(LaunchArgs a) {
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
   const uint32_t dl = (uint32_t)(Pr::d - a.shared_layers);

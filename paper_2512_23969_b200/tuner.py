@@ -172,6 +172,19 @@ def select_backends(profile_runs: dict, reps: int = 10, tie_tolerance: float = 0
     return out
 
 
+def pick_path(cell_ms: dict, names, tie_tolerance: float = 0.02) -> int:
+    """Variant id for one (kernel, set) cell of timings {path name: ms}: the
+    fastest compiled SHA-256 path, but a non-native path replaces native only
+    when it is faster by more than tie_tolerance (the reference's rule,
+    tuner.py:206-218, generalised from two backends to the compiled list)."""
+    names = list(names)
+    missing = [n for n in names if n not in cell_ms]
+    if missing:
+        raise TuningError(f"no timing for SHA-256 paths {missing}")
+    best = min(range(len(names)), key=lambda v: cell_ms[names[v]])
+    return best if cell_ms[names[best]] < cell_ms["native"] * (1.0 - tie_tolerance) else 0
+
+
 # ---------------------------------------------------------------------------
 # B200: the same search over the real kernel footprint, then device timing
 # ---------------------------------------------------------------------------
@@ -309,10 +322,7 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
                 var[kernel] = v
                 engine.set_config(set_id, variant=var)
                 cell[name] = _trimmed_mean(_kernel_ms(engine, set_id, count, kernel, reps))
-            # a non-native path replaces native only when faster by more than
-            # tie_tolerance (the reference's rule, tuner.py:206-218)
-            best_v = min(range(len(names)), key=lambda v: cell[names[v]])
-            variants[kernel] = best_v if cell[names[best_v]] < cell["native"] * (1.0 - tie_tolerance) else 0
+            variants[kernel] = pick_path(cell, names, tie_tolerance)
             vtable[kernel] = cell
         engine.set_config(set_id, variant=variants)
     # 3. multi-stream batching: T prioritised sub-batches per graph, timed end to

@@ -6,6 +6,7 @@ Acceptance values from the reference SPEC.
 from __future__ import annotations
 
 import json
+from pathlib import Path
 import random
 import threading
 
@@ -99,6 +100,31 @@ def test_config_roundtrip(tmp_path):
     bad["sets"]["128f"]["b200"]["fors_trees_per_set"] = 40
     with pytest.raises(ConfigError):
         TuningConfig.from_dict(bad)
+
+
+def test_pick_path_tie_rule():
+    names = ("native", "fast", "mx248")
+    assert tuner.pick_path({"native": 10.0, "fast": 9.0, "mx248": 8.0}, names) == 2
+    assert tuner.pick_path({"native": 10.0, "fast": 9.9, "mx248": 9.85}, names) == 0  # within 2 %: keep native
+    assert tuner.pick_path({"native": 10.0, "fast": 9.7, "mx248": 12.0}, names) == 1
+    with pytest.raises(TuningError):
+        tuner.pick_path({"native": 10.0}, names)
+
+
+def test_shipped_tuned_config_is_loadable_and_in_range():
+    """b200_tuned.json (the engine's default tuning) validates, and its SHA-path
+    ids and FORS / TREE_Sign shape fields are legal for the built library."""
+    from paper_2512_23969_b200 import _lib
+
+    path = Path(__file__).resolve().parent.parent / "paper_2512_23969_b200" / "b200_tuned.json"
+    cfg = TuningConfig.load(path)
+    cfg.validate()
+    n_paths = len(_lib.variant_names())
+    for set_id, row in cfg.sets.items():
+        b = row.b200
+        assert all(0 <= v < n_paths for v in b["variant"].values()), (set_id, b["variant"])
+        assert -1 <= b.get("fors_cta_levels", -1) <= derive(set_id).log_t
+        assert b.get("tree_split", True) in (True, False)
 
 
 class _FakeSigner:
