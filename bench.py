@@ -240,8 +240,9 @@ def measure_set(eng, info, set_id: str, count: int, steps: int, warmup: int, ran
     eng.stage(set_id, blob, offs, count)
     flush = 256 << 20
     cfg = eng.config(set_id)
-    shared_L = cfg["shared_layers"] if cfg["wots_from_tree"] else 0
     eng.bench_run(set_id, count, max(1, warmup), 0, flush)
+    shape = eng.batch_info(set_id)
+    shared_L = shape["shared_layers"]  # depth the auto policy chose for this batch
     launches0 = eng.launch_count
     eng.launch_stats(reset=True)
     barrier(dist)
@@ -264,8 +265,9 @@ def measure_set(eng, info, set_id: str, count: int, steps: int, warmup: int, ran
         plain_ms = eng.bench_run(set_id, count, steps, 0, flush)
         plain_s = max_over_ranks(dist, sum(plain_ms) / 1e3)
         value_plain = world * count * steps / plain_s
-        eng.set_config(set_id, shared_layers=shared_L)
+        eng.set_config(set_id, shared_layers=cfg["shared_layers"])
         eng.stage(set_id, blob, offs, count)
+        assert eng.batch_info(set_id)["shared_layers"] == shared_L
 
     # ---- per-kernel roofline (serialised run, CUDA events around each kernel) ----
     eng.bench_run(set_id, count, 1, 1, flush)
@@ -406,6 +408,7 @@ def run_ours(args):
                 "value": round(o["value"], 1), "unit": "sig/s", "messages_per_gpu": n,
                 "ms_per_step": round(1e3 * o["dev_s"] / min(args.steps, 5), 4),
                 "value_no_subtree_sharing": round(o["value_plain"], 1) if o["value_plain"] else None,
+                "subtree_sharing_layers": o["shared_L"],
                 "e2e": o["e2e"], "launch_latency": o["launch_latency"],
                 "roofline": {k: o["roofline"][k] for k in ("achieved", "peak", "unit", "frac", "kernel_ms")},
                 "clocks": {"sm_mhz": o["clk"]["sm_mhz"], "reasons": o["clk"]["reasons"]},
@@ -452,6 +455,8 @@ def run_ours(args):
             "launch_latency": r["launch_latency"],
             "value_no_subtree_sharing": round(r["value_plain"], 1) if r["value_plain"] else None,
             "subtree_sharing": {"layers": r["shared_L"], "shared_subtrees_per_key": r["units"],
+                                "policy": "shared_auto: a top layer is shared when its subtrees per key are at most "
+                                          "half the key's messages (max 5 layers; 4 for 256f)",
                                 "note": "top hypertree layers address few subtrees per key; each distinct "
                                         "(key, layer, tree) subtree is computed once per batch (bytes unchanged)"},
             "roofline": r["roofline"],

@@ -74,7 +74,7 @@ typedef struct {
   int32_t shared_layers;      /* top hypertree layers whose subtrees are
                                  computed once per (key, tree) per batch
                                  instead of once per message (0 = off; max
-                                 4 for 128f/192f, 3 for 256f)                */
+                                 5 for 128f/192f, 4 for 256f)                */
   int32_t shared_auto;        /* 1: per batch, share a layer only when its
                                  shareable subtrees are fewer than half the
                                  messages (and within the table budget);
@@ -156,6 +156,12 @@ HS_API int hs_bench_run(hs_t *h, int set, uint32_t count, int32_t steps, int mod
 
 /* Kernel launches issued by this handle since open (for bench accounting). */
 HS_API int64_t hs_launch_count(hs_t *h);
+
+/* Shape of the staged batch as the engine will run it: out[0] staged
+ * messages, out[1] subtree-sharing depth chosen for it (shared_auto policy),
+ * out[2] FORS levels kept in the CTA (fors_cta_levels resolved), out[3]
+ * tree_split.  Returns the number of values written. */
+HS_API int hs_batch_info(hs_t *h, int set, int32_t *out, int cap);
 
 /* SHA-256 arithmetic paths compiled into this library (hs_set_config.variant
  * ids): returns their number n; id 0 is the native path, id 1 the fast path,

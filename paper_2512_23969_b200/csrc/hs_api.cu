@@ -385,7 +385,7 @@ cudaError_t enqueue_fors(int set, const hs_set_config& c, const LaunchArgs& a, c
 
 // Config-dependent scratch for `count` messages: upper FORS levels and the
 // split TREE_Sign's chain ends.
-int ensure_fors_nodes(hs_t* h, int set, uint32_t count) {
+int ensure_scratch(hs_t* h, int set, uint32_t count) {
   Buffers& B = h->buf[set];
   const hs_set_config& c = h->sets[set].cfg;
   void* before[3] = {B.fnodes[0], B.fnodes[1], B.ends};
@@ -516,7 +516,7 @@ int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nu
   h->last_set = set;
   h->last_mode = mode;
   const size_t sb = (size_t)kInfo[set].sig_bytes;
-  if (int rc = ensure_fors_nodes(h, set, std::max(count, St.staged)); rc != HS_OK) return rc;
+  if (int rc = ensure_scratch(h, set, std::max(count, St.staged)); rc != HS_OK) return rc;
   if (mode == 1) {  // serialised kernels with per-kernel events (roofline timing)
     CUDA_TRY(h, enqueue(h, set, make_args(h, set, 0, count), false, true));
     if (fetch_to)
@@ -993,6 +993,15 @@ int hs_bench_run(hs_t* h, int set, uint32_t count, int32_t steps, int mode, uint
 }
 
 int64_t hs_launch_count(hs_t* h) { return h ? h->launches : -1; }
+
+int hs_batch_info(hs_t* h, int set, int32_t* out, int cap) {
+  if (!h || !valid_set(set) || (cap > 0 && !out)) return fail(h, HS_E_USAGE, "bad arguments");
+  const SetState& St = h->sets[set];
+  const int32_t v[4] = {(int32_t)St.staged, St.shared_eff, fors_cta_levels(set, St.cfg), St.cfg.tree_split};
+  const int n = std::min(cap, 4);
+  for (int i = 0; i < n; i++) out[i] = v[i];
+  return n;
+}
 
 int hs_variants(int32_t* masks, int cap) {
   const int nm = hs::kVariants - 2;

@@ -499,7 +499,9 @@ __global__ void __launch_bounds__(kTreeBlock) tree_root_kernel(LaunchArgs a) {
 template <int S>
 struct Shared {
   using Pr = P<S>;
-  static constexpr int max_layers = Pr::hp >= 4 ? 3 : 4;
+  // one layer deeper than the 2^(hp*j) units reach ~4096 per key: the auto
+  // policy shares it only for batches of >= 8192 messages per key
+  static constexpr int max_layers = Pr::hp >= 4 ? 4 : 5;
   static constexpr int node_words = (2 * Pr::leaves - 1) * 8;
   static constexpr int leaf_stash_words = Pr::wots_len * Pr::w * Pr::NW;
   static constexpr int rec_words = node_words + Pr::leaves * leaf_stash_words;
