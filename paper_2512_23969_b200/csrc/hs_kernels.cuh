@@ -360,13 +360,18 @@ __global__ void __launch_bounds__(kTreeBlock, (S == 2 ? kTreeMinBlocks8 : kTreeM
 #ifndef HS_CHAIN_BLOCK
 #define HS_CHAIN_BLOCK 128
 #endif
-#ifndef HS_CHAIN_MIN_BLOCKS
-#define HS_CHAIN_MIN_BLOCKS 1
-#endif
 constexpr int kChainBlock = HS_CHAIN_BLOCK;
+// No min-blocks bound by default: ptxas then allocates 55-64 registers for the
+// chain loop; any explicit bound (even 1) changes the allocation and cost
+// 5-10 % on B200 (profiles/r01_chain_block_sweep.txt).
+#ifdef HS_CHAIN_MIN_BLOCKS
+#define HS_CHAIN_BOUNDS __launch_bounds__(kChainBlock, HS_CHAIN_MIN_BLOCKS)
+#else
+#define HS_CHAIN_BOUNDS __launch_bounds__(kChainBlock)
+#endif
 
 template <int S, class V>
-__global__ void __launch_bounds__(kChainBlock, HS_CHAIN_MIN_BLOCKS) tree_chain_kernel(LaunchArgs a) {
+__global__ void HS_CHAIN_BOUNDS tree_chain_kernel(LaunchArgs a) {
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
   const uint32_t dl = (uint32_t)(Pr::d - a.shared_layers);
