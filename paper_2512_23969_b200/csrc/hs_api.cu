@@ -59,6 +59,15 @@ size_t shared_words(int set, int layers) {
   return 0;
 }
 
+size_t shared_end_words(int set, int layers) {
+  switch (set) {
+    case 0: return shared_end_words_per_key<0>(layers);
+    case 1: return shared_end_words_per_key<1>(layers);
+    case 2: return shared_end_words_per_key<2>(layers);
+  }
+  return 0;
+}
+
 int shared_max(int set) {
   switch (set) {
     case 0: return shared_max_layers<0>();
@@ -145,6 +154,7 @@ struct Buffers {
   uint8_t* key_used = nullptr; size_t key_used_cap = 0;
   uint32_t* fnodes[2] = {nullptr, nullptr}; size_t fnodes_cap[2] = {0, 0};  // upper FORS levels
   uint32_t* ends = nullptr; size_t ends_cap = 0;  // split TREE_Sign chain ends
+  uint32_t* sends = nullptr; size_t sends_cap = 0;  // split shared-subtree chain ends
   // pinned staging
   uint8_t* h_msgs = nullptr; size_t h_msgs_cap = 0;
   uint64_t* h_offs = nullptr; size_t h_offs_cap = 0;
@@ -351,10 +361,24 @@ LaunchArgs make_args(hs_t* h, int set, uint32_t first, uint32_t count) {
     a.shared = B.shared;
     a.shared_layers = L;
     a.key_used = B.key_used;
+    if (St.cfg.tree_split && B.sends && B.sends_cap >= (size_t)St.nkeys * shared_end_words(set, L))
+      a.shared_ends = B.sends;
   }
   if (St.cfg.tree_split && B.ends && B.ends_cap >= chain_end_words(set, first + count))
     a.chain_ends = B.ends + (size_t)first * (I.d - a.shared_layers) * I.leaves * I.wots_len * (I.n / 4);
   return a;
+}
+
+// Shared top-layer subtrees on one stream: split (chain grid, then leaf grid) or fused.
+cudaError_t enqueue_shared(int set, const hs_set_config& c, const LaunchArgs& a, cudaStream_t s, int& kernels) {
+  if (a.shared_layers <= 0) return cudaSuccess;
+  if (!a.shared_ends) {
+    kernels++;
+    return launch(set, K_TREE_SHARED, c.variant[1], a, s);
+  }
+  kernels += 2;
+  cudaError_t e = launch(set, K_SHARED_CHAIN, c.variant[1], a, s);
+  return e == cudaSuccess ? launch(set, K_SHARED_ROOT, c.variant[1], a, s) : e;
 }
 
 // TREE_Sign on one stream: split (chain grid, then leaf / Merkle grid) or fused.
@@ -409,7 +433,7 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
   };
   cudaError_t e;
 #define TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
-  int kernels = 2 + (a.shared_layers > 0 ? 1 : 0);  // + the FORS / TREE branches, counted by enqueue_*
+  int kernels = 2;  // msg_prep + WOTS; the shared / FORS / TREE branches are counted by enqueue_*
   TRY(rec(0, h->s0));
   if (a.shared_layers > 0) TRY(cudaMemsetAsync(a.key_used, 0, a.nkeys, h->s0));
   TRY(launch(set, K_PREP, c.variant[3], a, h->s0));
@@ -419,7 +443,7 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
     TRY(rec(2, h->s0));
     TRY(enqueue_tree(set, c, a, h->s0, kernels));
     TRY(rec(3, h->s0));  // [2,3] = per-message TREE_Sign only (the roofline kernel)
-    if (a.shared_layers > 0) TRY(launch(set, K_TREE_SHARED, c.variant[1], a, h->s0));
+    TRY(enqueue_shared(set, c, a, h->s0, kernels));
     TRY(rec(5, h->s0));
     TRY(launch(set, a.stash ? K_WOTS_GATHER : K_WOTS, c.variant[2], a, h->s0));
     TRY(rec(4, h->s0));
@@ -429,7 +453,7 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
     // the shared-subtree kernel is small and latency bound (a few subtrees,
     // one thread per leaf): start it first on the FORS branch so it runs
     // under the per-message TREE_Sign instead of after it
-    if (a.shared_layers > 0) TRY(launch(set, K_TREE_SHARED, c.variant[1], a, h->s1));
+    TRY(enqueue_shared(set, c, a, h->s1, kernels));
     TRY(enqueue_fors(set, c, a, h->s1, kernels));
     TRY(rec(2, h->s1));
     TRY(cudaEventRecord(h->join, h->s1));
@@ -476,9 +500,8 @@ cudaError_t enqueue_batch(hs_t* h, int set, uint32_t count, int T, bool capture)
   TRY(cudaEventRecord(h->fork, h->s0));
   if (all.shared_layers > 0) {
     TRY(cudaStreamWaitEvent(h->q[0], h->fork, 0));
-    TRY(launch(set, K_TREE_SHARED, c.variant[1], all, h->q[0]));
+    TRY(enqueue_shared(set, c, all, h->q[0], kernels));
     TRY(cudaEventRecord(h->sh_done, h->q[0]));
-    kernels++;
   }
   const uint32_t per = (count + T - 1) / T;
   for (int j = 0; j < T; j++) {
@@ -623,10 +646,12 @@ int stage_inputs(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, co
   }
   if (St.shared_eff > 0) {
     const size_t need = (size_t)St.nkeys * shared_words(set, St.shared_eff);
-    void* before[2] = {B.shared, B.key_used};
+    void* before[3] = {B.shared, B.key_used, B.sends};
     CUDA_TRY(h, grow(B.shared, B.shared_cap, need));
     CUDA_TRY(h, grow(B.key_used, B.key_used_cap, (size_t)St.nkeys));
-    void* after[2] = {B.shared, B.key_used};
+    if (St.cfg.tree_split)
+      CUDA_TRY(h, grow(B.sends, B.sends_cap, (size_t)St.nkeys * shared_end_words(set, St.shared_eff)));
+    void* after[3] = {B.shared, B.key_used, B.sends};
     if (std::memcmp(before, after, sizeof before) != 0) {
       B.gen++;
       drop_graphs(h);
@@ -708,6 +733,7 @@ void hs_close(hs_t* h) {
     cudaFree(B.fnodes[0]);
     cudaFree(B.fnodes[1]);
     cudaFree(B.ends);
+    cudaFree(B.sends);
     cudaFree(h->sets[s].sk_raw);
   }
   if (h->flush) cudaFree(h->flush);

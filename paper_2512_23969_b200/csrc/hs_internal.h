@@ -26,6 +26,8 @@ enum KernelId : int {
   K_FORS_LEVEL = 10,
   K_TREE_CHAIN = 11,
   K_TREE_ROOT = 12,
+  K_SHARED_CHAIN = 13,
+  K_SHARED_ROOT = 14,
 };
 
 // variant: SHA-256 arithmetic path id, 0..kNumVariants-1 (sha256.cuh VariantOf)
@@ -47,5 +49,9 @@ size_t shared_words_per_key(int layers);
 
 template <int S>
 int shared_max_layers();
+
+// words of the split shared-subtree chain-end buffer per key for `layers`
+template <int S>
+size_t shared_end_words_per_key(int layers);
 
 }  // namespace hs

@@ -83,6 +83,7 @@ struct LaunchArgs {
   // compresses them into leaves and reduces the subtrees.  nullptr = fused
   // tree_sign_kernel (thread = leaf runs its own chains).
   uint32_t* chain_ends;
+  uint32_t* shared_ends;     // split shared subtrees: [key][unit][leaf][chain][NW] (nullable)
 };
 
 __device__ __forceinline__ uint64_t shr64(uint64_t x, int s) { return s >= 64 ? 0ull : (x >> s); }
@@ -547,6 +548,117 @@ __global__ void __launch_bounds__(kTreeBlock, (S == 2 ? kTreeMinBlocks8 : kTreeM
     R = Sh::rec(a, key, (int)layer, tree);
     wots_leaf<S, V>(K, layer, tree, leaf, &tbuf[threadIdx.x], kTreeBlock, node,
                     R + Sh::node_words + (size_t)leaf * Sh::leaf_stash_words);
+#pragma unroll
+    for (int w = 0; w < NW; w++) R[leaf * 8 + w] = node[w];
+  }
+#pragma unroll 1
+  for (int lvl = 1; lvl <= Pr::hp; lvl++) {
+    uint32_t other[NW];
+#pragma unroll
+    for (int w = 0; w < NW; w++) other[w] = __shfl_down_sync(0xffffffffu, node[w], 1u << (lvl - 1));
+    if (valid && (leaf & ((1u << lvl) - 1u)) == 0u) {
+      uint32_t m[2 * NW], mid[8];
+#pragma unroll
+      for (int w = 0; w < NW; w++) { m[w] = node[w]; m[NW + w] = other[w]; }
+#pragma unroll
+      for (int w = 0; w < 8; w++) mid[w] = K.thash_mid[w];
+      thash_reg<V, 2 * NW>(node, mid, make_adrs(layer, tree, ADDR_HASHTREE, 0, (uint32_t)lvl, leaf >> lvl), m);
+      uint32_t* dst = R + (size_t)(Sh::level_off(lvl) + (leaf >> lvl)) * 8;
+#pragma unroll
+      for (int w = 0; w < NW; w++) dst[w] = node[w];
+    }
+  }
+}
+
+// Split form of tree_shared_kernel (used with tree_split): the shared
+// subtrees' chains as one grid (thread = (key, unit, leaf, chain), every
+// position recorded into the subtree record for the WOTS gather), then one
+// thread per (key, unit, leaf) for T_len and the record's Merkle levels.  The
+// fused kernel runs a whole leaf per thread with only units x leaves threads
+// (4,681 x 8 for 128f/192f at 5 shared layers), a long serial tail under the
+// per-message kernels; the split grids have wots_len times more threads.
+// Bodies follow tree_chain_kernel / tree_root_kernel (kept separate so the
+// per-message kernels' register allocation is untouched).
+template <int S>
+__device__ __forceinline__ bool shared_coords(const LaunchArgs& a, uint64_t lid, uint32_t& key, uint32_t& layer,
+                                              uint64_t& tree, uint32_t& leaf) {
+  using Pr = P<S>;
+  using Sh = Shared<S>;
+  const uint64_t per_key = (uint64_t)Sh::units(a.shared_layers) * Pr::leaves;
+  key = (uint32_t)(lid / per_key);
+  if (key >= a.nkeys || !a.key_used[key]) return false;
+  const uint32_t rem = (uint32_t)(lid % per_key);
+  const uint32_t unit = rem / Pr::leaves;
+  leaf = rem % Pr::leaves;
+  int j = 0;
+  while (j + 1 < a.shared_layers && (uint32_t)Sh::units(j + 1) <= unit) j++;
+  layer = Pr::d - 1 - j;
+  tree = unit - Sh::units(j);
+  return true;
+}
+
+template <int S, class V>
+__global__ void HS_CHAIN_BOUNDS shared_chain_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  using Sh = Shared<S>;
+  constexpr int NW = Pr::NW;
+  const uint64_t gid = (uint64_t)blockIdx.x * kChainBlock + threadIdx.x;
+  if (gid >= (uint64_t)a.nkeys * Sh::units(a.shared_layers) * Pr::leaves * Pr::wots_len) return;
+  const uint32_t chain = (uint32_t)(gid % Pr::wots_len);
+  uint32_t key, layer, leaf;
+  uint64_t tree;
+  if (!shared_coords<S>(a, gid / Pr::wots_len, key, layer, tree, leaf)) return;
+  const KeyDev& K = a.keys[key];
+  uint32_t mid[8], sks[NW], st[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) mid[j] = K.thash_mid[j];
+#pragma unroll
+  for (int j = 0; j < NW; j++) sks[j] = K.sk_seed[j];
+  const Adrs wa = make_adrs(layer, tree, ADDR_WOTS, leaf, chain, 0);
+  prf_reg<V, NW>(st, sks, wa);
+  uint32_t x[NW];
+#pragma unroll
+  for (int j = 0; j < NW; j++) x[j] = st[j];
+  uint32_t* rec = Sh::rec(a, key, (int)layer, tree) + Sh::node_words + (size_t)leaf * Sh::leaf_stash_words +
+                  (size_t)chain * Pr::w * NW;
+#pragma unroll
+  for (int j = 0; j < NW; j++) rec[j] = x[j];
+  chain_F<V, NW>(x, mid, wa, 0u, (uint32_t)(Pr::w - 1), rec);
+  uint32_t* e = a.shared_ends + gid * NW;
+#pragma unroll
+  for (int j = 0; j < NW; j++) e[j] = x[j];
+}
+
+template <int S, class V>
+__global__ void __launch_bounds__(kTreeBlock) shared_root_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  using Sh = Shared<S>;
+  constexpr int NW = Pr::NW;
+  constexpr int M = Pr::wots_len * NW;
+  constexpr uint32_t total = 22u + (uint32_t)(Pr::wots_len * Pr::n);
+  constexpr uint32_t nblk = (total + 9u + 63u) / 64u;
+  const uint64_t gid = (uint64_t)blockIdx.x * kTreeBlock + threadIdx.x;
+  uint32_t key = 0, layer = 0, leaf = (uint32_t)(gid % Pr::leaves);
+  uint64_t tree = 0;
+  const bool valid = gid < (uint64_t)a.nkeys * Sh::units(a.shared_layers) * Pr::leaves &&
+                     shared_coords<S>(a, gid, key, layer, tree, leaf);
+  uint32_t node[8];
+  uint32_t* R = nullptr;
+  const KeyDev& K = a.keys[valid ? key : 0u];
+  if (valid) {
+    R = Sh::rec(a, key, (int)layer, tree);
+    const Adrs pa = make_adrs(layer, tree, ADDR_WOTS_PK, leaf, 0, 0);
+    const uint32_t aw[6] = {pa.w0, pa.w1, pa.w2, pa.w3, pa.w4, pa.h5};
+    const uint32_t* e = a.shared_ends + gid * M;
+#pragma unroll
+    for (int j = 0; j < 8; j++) node[j] = K.thash_mid[j];
+#pragma unroll 1
+    for (uint32_t b = 0; b < nblk; b++) {
+      uint32_t W[16];
+#pragma unroll
+      for (int j = 0; j < 16; j++) W[j] = tlen_word<M>(16u * b + j, aw, e, (64u + total) * 8u, 16u * nblk - 1u);
+      compress<V>(node, W);
+    }
 #pragma unroll
     for (int w = 0; w < NW; w++) R[leaf * 8 + w] = node[w];
   }

@@ -64,6 +64,12 @@ size_t shared_words_per_key<HS_SET>(int layers) {
 }
 
 template <>
+size_t shared_end_words_per_key<HS_SET>(int layers) {
+  using Pr = P<HS_SET>;
+  return (size_t)Shared<HS_SET>::units(layers) * Pr::leaves * Pr::wots_len * Pr::NW;
+}
+
+template <>
 int shared_max_layers<HS_SET>() {
   return Shared<HS_SET>::max_layers;
 }
