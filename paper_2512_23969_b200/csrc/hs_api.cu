@@ -470,6 +470,27 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
   return cudaSuccess;
 }
 
+// Messages [first, first + cn) of sub-batch j of T.  The last sub-batch gets
+// half the share of the others (weights 2, ..., 2, 1): only its D2H copy is
+// not hidden under later compute in hs_sign_batch, so it is kept small.
+void sub_range(uint32_t count, int T, int j, uint32_t& first, uint32_t& cn) {
+#ifdef HS_EQUAL_SUBBATCH
+  const uint32_t per = (count + T - 1) / T;
+  first = std::min(count, (uint32_t)j * per);
+  cn = std::min(per, count - first);
+#else
+  if (T <= 1) {
+    first = 0;
+    cn = count;
+    return;
+  }
+  const uint64_t W = 2ull * (uint64_t)T - 1ull;
+  auto edge = [&](int i) { return (uint32_t)((uint64_t)count * std::min<uint64_t>(2ull * (uint64_t)i, W) / W); };
+  first = edge(j);
+  cn = edge(j + 1) - first;
+#endif
+}
+
 // Multi-stream batch (the paper's m x T batching), one
 // graph per batch shape:
 //
@@ -503,11 +524,10 @@ cudaError_t enqueue_batch(hs_t* h, int set, uint32_t count, int T, bool capture)
     TRY(enqueue_shared(set, c, all, h->q[0], kernels));
     TRY(cudaEventRecord(h->sh_done, h->q[0]));
   }
-  const uint32_t per = (count + T - 1) / T;
   for (int j = 0; j < T; j++) {
-    const uint32_t first = (uint32_t)j * per;
-    if (first >= count) break;
-    const uint32_t cn = std::min(per, count - first);
+    uint32_t first, cn;
+    sub_range(count, T, j, first, cn);
+    if (cn == 0) break;
     const LaunchArgs a = make_args(h, set, first, cn);
     // TREE_j on priority 1+2j, FORS_j just below it: FORS_j's short CTAs fill
     // the SMs TREE_j drains before TREE_{j+1} claims them, and the last
@@ -580,11 +600,10 @@ int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nu
     CUDA_TRY(h, enqueue_batch(h, set, count, T, false));
   }
   if (fetch_to) {
-    const uint32_t per = (count + T - 1) / T;
     for (int j = 0; j < T; j++) {
-      const uint32_t first = (uint32_t)j * per;
-      if (first >= count) break;
-      const uint32_t cn = std::min(per, count - first);
+      uint32_t first, cn;
+      sub_range(count, T, j, first, cn);
+      if (cn == 0) break;
       CUDA_TRY(h, cudaStreamWaitEvent(h->ls[j], h->done[j], 0));
       CUDA_TRY(h, cudaMemcpyAsync(fetch_to + first * sb, h->buf[set].sigs + first * sb, cn * sb,
                                   cudaMemcpyDeviceToHost, h->ls[j]));
