@@ -114,10 +114,11 @@ def lib() -> ctypes.CDLL:
 
 def variant_names() -> tuple[str, ...]:
     """Names of the SHA-256 paths compiled into the loaded library (hs_variants):
-    ("native", "fast", "mx<mask>", ...), indexed by hs_set_config.variant id."""
+    ("native", "fast", "mx<mask>[p<order>]", ...), indexed by hs_set_config.variant id."""
     buf = (ctypes.c_int32 * 64)()
     n = lib().hs_variants(buf, 64)
-    return ("native", "fast") + tuple(f"mx{buf[i]}" for i in range(n - 2))
+    return ("native", "fast") + tuple(f"mx{buf[i] & 255}" + (f"p{buf[i] >> 8}" if buf[i] >> 8 else "")
+                                      for i in range(n - 2))
 
 
 def check(handle, rc: int, what: str) -> None:

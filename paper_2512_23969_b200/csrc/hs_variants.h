@@ -1,6 +1,6 @@
 // hs_variants.h -- which SHA-256 arithmetic paths the library is built with.
-// Variant id 0 = Native, 1 = Fast, 2.. = sha256.cuh Mx<mask> for each mask
-// below (override with make MASKS=...; tools/sha_sweep and
+// Variant id 0 = Native, 1 = Fast, 2.. = sha256.cuh Mx<mask, order> for each
+// code below (code = mask + 256 * operand order) (override with make MASKS=...; tools/sha_sweep and
 // tools/variant_sweep.py choose them from B200 timings of the real kernels).
 #pragma once
 #ifndef HS_MX_MASKS

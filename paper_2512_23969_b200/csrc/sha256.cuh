@@ -173,15 +173,23 @@ using Fast = Mix<0, 0, 0, true, 1, true, false>;
 // instead of 1 per cycle); which split wins depends on ptxas's register
 // assignment for the surrounding kernel, so the engine compiles a few masks
 // and the on-device tuner times them per (kernel, set).
-template <int B>
+// P (operand order, tools/perm_sweep): bit0 T1 = IMAD(IMAD(hk, S1), IMAD(w, Ch))
+// (with T1 form 3), bit1 a' = IMAD(IMAD(T1, S0), Maj), bit2 W = IMAD(IMAD(IMAD(
+// s1, w16), w7), s0) (with bit6), bit3 Sigma rotations in reverse order.  Same
+// arithmetic; ptxas's schedule and register assignment change with the order.
+template <int B, int P = 0>
 struct Mx : Native {
-  static constexpr int id = 100 + B;
+  static constexpr int id = 100 + B + 256 * P;
   static constexpr int T1F = (B >> 3) & 3;
   static __device__ __forceinline__ uint32_t S0(uint32_t a) {
-    return ((B & 2) ? fma_rotr(a, 2) : rotr(a, 2)) ^ rotr(a, 13) ^ rotr(a, 22);
+    const uint32_t r2 = (B & 2) ? fma_rotr(a, 2) : rotr(a, 2);
+    if (P & 8) return rotr(a, 22) ^ rotr(a, 13) ^ r2;
+    return r2 ^ rotr(a, 13) ^ rotr(a, 22);
   }
   static __device__ __forceinline__ uint32_t S1(uint32_t e) {
-    return ((B & 1) ? fma_rotr(e, 6) : rotr(e, 6)) ^ rotr(e, 11) ^ rotr(e, 25);
+    const uint32_t r6 = (B & 1) ? fma_rotr(e, 6) : rotr(e, 6);
+    if (P & 8) return rotr(e, 25) ^ rotr(e, 11) ^ r6;
+    return r6 ^ rotr(e, 11) ^ rotr(e, 25);
   }
   static __device__ __forceinline__ uint32_t s0(uint32_t x) {
     return rotr(x, 7) ^ rotr(x, 18) ^ ((B & 4) ? fma_shr(x, 3) : (x >> 3));
@@ -193,23 +201,27 @@ struct Mx : Native {
     if (T1F == 0) return h + k + w + s1v + chv;
     if (T1F == 1) return fma_add(h + k + w, fma_add(s1v, chv));
     if (T1F == 2) return fma_add(fma_add(fma_add(w, h), k), fma_add(s1v, chv));
+    if (P & 1) return fma_add(fma_add(fma_addk(h, k), s1v), fma_add(w, chv));
     return fma_add(fma_add(w, fma_addk(h, k)), fma_add(s1v, chv));
   }
   static __device__ __forceinline__ uint32_t enew(uint32_t d, uint32_t t) { return (B & 128) ? fma_add(d, t) : d + t; }
   static __device__ __forceinline__ uint32_t anew(uint32_t t, uint32_t s0v, uint32_t mj) {
-    return (B & 32) ? fma_add(t, fma_add(s0v, mj)) : t + s0v + mj;
+    if (!(B & 32)) return t + s0v + mj;
+    return (P & 2) ? fma_add(fma_add(t, s0v), mj) : fma_add(t, fma_add(s0v, mj));
   }
   static __device__ __forceinline__ uint32_t wnew(uint32_t s1v, uint32_t w7, uint32_t s0v, uint32_t w16) {
-    return (B & 64) ? fma_add(fma_add(s1v, w7), fma_add(s0v, w16)) : fma_add(s1v + w7 + s0v, w16);
+    if (!(B & 64)) return fma_add(s1v + w7 + s0v, w16);
+    return (P & 4) ? fma_add(fma_add(fma_add(s1v, w16), w7), s0v) : fma_add(fma_add(s1v, w7), fma_add(s0v, w16));
   }
   static __device__ __forceinline__ uint32_t ff(uint32_t x, uint32_t y) { return x + y; }
 };
 
 // Engine variant ids (hs_set_config.variant): 0 Native, 1 Fast, then one Mx
-// per mask of HS_MX_MASKS (hs_variants.h; set at build time).
+// per code of HS_MX_MASKS (hs_variants.h; set at build time); code = mask B +
+// 256 * operand order P.
 constexpr int kMxMasks[] = {HS_MX_MASKS};
 constexpr int kNumVariants = 2 + (int)(sizeof(kMxMasks) / sizeof(kMxMasks[0]));
-template <int ID> struct VariantOf { using T = Mx<kMxMasks[ID - 2]>; };
+template <int ID> struct VariantOf { using T = Mx<(kMxMasks[ID - 2] & 255), (kMxMasks[ID - 2] >> 8)>; };
 template <> struct VariantOf<0> { using T = Native; };
 template <> struct VariantOf<1> { using T = Fast; };
 

@@ -142,5 +142,5 @@ def test_compiled_sha_paths(L):
     default = re.search(r"#define HS_MX_MASKS ([\d, ]+)", hdr).group(1)
     masks = [int(x) for x in default.split(",")]
     if not os.environ.get("HERO_SIGN_LIB"):
-        assert names[2:] == tuple(f"mx{m}" for m in masks)
-    assert all(0 <= int(n[2:]) < 256 for n in names[2:])
+        assert names[2:] == tuple(f"mx{m & 255}" + (f"p{m >> 8}" if m >> 8 else "") for m in masks)
+    assert all(re.fullmatch(r"mx\d+(p\d+)?", n) for n in names[2:])
