@@ -184,7 +184,15 @@ class Engine:
                 raise UsageError("key_idx must hold one entry per message")
         orand = None
         if opt_rand is not None:
-            orand = opt_rand if isinstance(opt_rand, (bytes, bytearray)) else b"".join(opt_rand)
+            if isinstance(opt_rand, (bytes, bytearray)):
+                orand = opt_rand
+            else:
+                # a None entry means the reference default, PK.seed of the message's key (sigcore.py:162-163)
+                ks = self._keys[set_id]
+                kk = kidx if kidx is not None else np.zeros(count, dtype=np.uint32)
+                orand = b"".join(o if o is not None else ks[int(kk[i]) * p.sk_bytes + 2 * p.n:
+                                                          int(kk[i]) * p.sk_bytes + 3 * p.n]
+                                 for i, o in enumerate(opt_rand))
             if len(orand) != count * p.n:
                 raise UsageError(f"opt_rand must be {p.n} bytes per message")
             orand = bytes(orand)

@@ -62,3 +62,28 @@ def test_batch_sizes_and_graph_replay(eng, oracle_mod, count):
     ref, _ = oracle_mod.sign_many("128f", sk, None, [msgs[i] for i in check])
     assert [first[i] for i in check] == ref
     assert all(eng.verify_batch("128f", sk[32:], msgs, first))
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_chunked_multistream_mixed_keys(eng, oracle_mod, set_id):
+    """hs_sign_batch over several chunks (chunk < count), 4 weighted sub-batches
+    per chunk, two keys, mixed opt_rand: every signature equals the oracle's."""
+    p = derive(set_id)
+    rng = random.Random(4242 + p.n)
+    sks = [oracle_mod.keygen(set_id, rng.randbytes(3 * p.n)) for _ in range(2)]
+    count = 2600 if set_id == "128f" else 1100
+    msgs = [rng.randbytes(rng.choice([0, 32, 100])) for _ in range(count)]
+    kidx = [rng.randrange(2) for _ in range(count)]
+    opts = [rng.randbytes(p.n) if i % 5 == 0 else None for i in range(count)]
+    eng.upload_keys(set_id, sks)
+    base = eng.config(set_id)
+    try:
+        eng.set_config(set_id, chunk=1024, streams=4)
+        sigs = eng.sign_batch(set_id, msgs, key_idx=kidx, opt_rand=opts)
+    finally:
+        eng.set_config(set_id, **base)
+    # oracle: opt_rand None means PK.seed (sigcore.py:162-163)
+    blob = b"".join(o if o is not None else sks[k][2 * p.n:3 * p.n] for o, k in zip(opts, kidx))
+    ref, _ = oracle_mod.sign_many(set_id, b"".join(sks), kidx, msgs, blob)
+    bad = [i for i in range(count) if sigs[i] != ref[i]]
+    assert not bad, bad[:10]
