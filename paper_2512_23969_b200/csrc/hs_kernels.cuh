@@ -34,6 +34,7 @@ struct KeyDev {
   uint32_t thash_mid[8];  // compress(IV, pk_seed || 0^(64-n))
   uint32_t hmac_i[8];     // compress(IV, (sk_prf||0) ^ 0x36..)
   uint32_t hmac_o[8];     // compress(IV, (sk_prf||0) ^ 0x5c..)
+  uint32_t prf_mid[8];    // SHA-256 state after rounds 0..NW-1 over SK.seed: every PRF of the key resumes here
 };
 
 struct MsgPlan {
@@ -126,6 +127,8 @@ __global__ void key_setup_kernel(LaunchArgs a) {
   for (int j = 0; j < 8; j++) kd.hmac_o[j] = IVc(j);
   for (int j = 0; j < 16; j++) W[j] = (j < Pr::NW ? kd.sk_prf[j] : 0u) ^ 0x5c5c5c5cu;
   compress<V>(kd.hmac_o, W);
+  for (int j = 0; j < 8; j++) kd.prf_mid[j] = IVc(j);
+  rounds_prefix<V, Pr::NW>(kd.prf_mid, kd.sk_seed);
   a.keys_out[i] = kd;
 }
 
@@ -394,7 +397,7 @@ __global__ void HS_CHAIN_BOUNDS tree_chain_kernel(LaunchArgs a) {
 #pragma unroll
   for (int j = 0; j < NW; j++) sks[j] = K.sk_seed[j];
   const Adrs wa = make_adrs(layer, tree, ADDR_WOTS, leaf, chain, 0);
-  prf_reg<V, NW>(st, sks, wa);                          // chain secret (wots.py:63-65)
+  prf_keyed<V, NW>(st, K.prf_mid, sks, wa);             // chain secret (wots.py:63-65)
   uint32_t x[NW];
 #pragma unroll
   for (int j = 0; j < NW; j++) x[j] = st[j];
@@ -615,7 +618,7 @@ __global__ void HS_CHAIN_BOUNDS shared_chain_kernel(LaunchArgs a) {
 #pragma unroll
   for (int j = 0; j < NW; j++) sks[j] = K.sk_seed[j];
   const Adrs wa = make_adrs(layer, tree, ADDR_WOTS, leaf, chain, 0);
-  prf_reg<V, NW>(st, sks, wa);
+  prf_keyed<V, NW>(st, K.prf_mid, sks, wa);
   uint32_t x[NW];
 #pragma unroll
   for (int j = 0; j < NW; j++) x[j] = st[j];
@@ -1021,7 +1024,7 @@ __global__ void __launch_bounds__(kSmallBlock) wots_sign_kernel(LaunchArgs a) {
   for (int j = 0; j < NW; j++) sks[j] = K.sk_seed[j];
   Adrs wa = make_adrs((uint32_t)layer, tree, ADDR_WOTS, leaf, (uint32_t)chain, 0);
   uint32_t st[8];
-  prf_reg<V, NW>(st, sks, wa);
+  prf_keyed<V, NW>(st, K.prf_mid, sks, wa);
   uint32_t x[NW];
 #pragma unroll
   for (int j = 0; j < NW; j++) x[j] = st[j];

@@ -439,6 +439,24 @@ __device__ __forceinline__ void prf_reg(uint32_t st[8], const uint32_t* sk_seed,
   compress<V>(st, W);
 }
 
+// PRF resumed from the key's state after rounds 0..NW-1 (those rounds read
+// only SK.seed, identical for every PRF of the key; KeyDev::prf_mid).
+template <class V, int NW>
+__device__ __forceinline__ void prf_keyed(uint32_t st[8], const uint32_t prf_mid[8], const uint32_t* sk_seed,
+                                          const Adrs& a) {
+  uint32_t W[16], sR[8];
+#pragma unroll
+  for (int j = 0; j < NW; j++) W[j] = sk_seed[j];
+  W[NW + 0] = a.w0; W[NW + 1] = a.w1; W[NW + 2] = a.w2; W[NW + 3] = a.w3; W[NW + 4] = a.w4;
+  W[NW + 5] = (a.h5 << 16) | 0x8000u;
+#pragma unroll
+  for (int j = NW + 6; j < 15; j++) W[j] = 0;
+  W[15] = (uint32_t)((4 * NW + 22) * 8);
+#pragma unroll
+  for (int i = 0; i < 8; i++) { st[i] = IVc(i); sR[i] = prf_mid[i]; }
+  compress_resume<V, NW>(st, sR, W);
+}
+
 // ---------------------------------------------------------------------------
 // Streaming tweakable hash over many nodes (T_len, T_k).  Message words go
 // into a 32-word ring (two SHA blocks) in a caller-provided column of shared
