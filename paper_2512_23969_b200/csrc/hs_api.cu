@@ -155,6 +155,7 @@ struct Buffers {
   uint32_t* fnodes[2] = {nullptr, nullptr}; size_t fnodes_cap[2] = {0, 0};  // upper FORS levels
   uint32_t* ends = nullptr; size_t ends_cap = 0;  // split TREE_Sign chain ends
   uint32_t* sends = nullptr; size_t sends_cap = 0;  // split shared-subtree chain ends
+  uint32_t* lpre = nullptr; size_t lpre_cap = 0;    // per-message, per-FORS-level H prefix states
   // pinned staging
   uint8_t* h_msgs = nullptr; size_t h_msgs_cap = 0;
   uint64_t* h_offs = nullptr; size_t h_offs_cap = 0;
@@ -347,9 +348,11 @@ LaunchArgs make_args(hs_t* h, int set, uint32_t first, uint32_t count) {
   a.fors_sets_fused = St.cfg.fors_sets_fused;
   a.fors_relax = St.cfg.fors_relax;
   a.fors_cta_levels = fors_cta_levels(set, St.cfg);
-  if (a.fors_cta_levels < I.log_t)
+  if (a.fors_cta_levels < I.log_t) {
     for (int b = 0; b < 2; b++)
       a.fors_nodes[b] = B.fnodes[b] + (size_t)first * I.k * ((size_t)I.t >> (a.fors_cta_levels + b)) * (I.n / 4);
+    a.fors_lpre = B.lpre + (size_t)first * (I.log_t + 1) * 8;
+  }
   const size_t sw = stash_words(set);
   a.stash = (St.cfg.wots_from_tree && B.stash && B.stash_cap >= ((size_t)first + count) * sw)
                 ? B.stash + (size_t)first * sw
@@ -412,11 +415,13 @@ cudaError_t enqueue_fors(int set, const hs_set_config& c, const LaunchArgs& a, c
 int ensure_scratch(hs_t* h, int set, uint32_t count) {
   Buffers& B = h->buf[set];
   const hs_set_config& c = h->sets[set].cfg;
-  void* before[3] = {B.fnodes[0], B.fnodes[1], B.ends};
-  if (fors_node_words(set, c, count, 0) != 0)
+  void* before[4] = {B.fnodes[0], B.fnodes[1], B.ends, B.lpre};
+  if (fors_node_words(set, c, count, 0) != 0) {
     for (int b = 0; b < 2; b++) CUDA_TRY(h, grow(B.fnodes[b], B.fnodes_cap[b], fors_node_words(set, c, count, b)));
+    CUDA_TRY(h, grow(B.lpre, B.lpre_cap, (size_t)count * (kInfo[set].log_t + 1) * 8));
+  }
   if (c.tree_split) CUDA_TRY(h, grow(B.ends, B.ends_cap, chain_end_words(set, count)));
-  void* after[3] = {B.fnodes[0], B.fnodes[1], B.ends};
+  void* after[4] = {B.fnodes[0], B.fnodes[1], B.ends, B.lpre};
   if (std::memcmp(before, after, sizeof before) != 0) {
     B.gen++;
     drop_graphs(h);
@@ -753,6 +758,7 @@ void hs_close(hs_t* h) {
     cudaFree(B.fnodes[1]);
     cudaFree(B.ends);
     cudaFree(B.sends);
+    cudaFree(B.lpre);
     cudaFree(h->sets[s].sk_raw);
   }
   if (h->flush) cudaFree(h->flush);

@@ -85,6 +85,7 @@ struct LaunchArgs {
   // tree_sign_kernel (thread = leaf runs its own chains).
   uint32_t* chain_ends;
   uint32_t* shared_ends;     // split shared subtrees: [key][unit][leaf][chain][NW] (nullable)
+  uint32_t* fors_lpre;       // [msg][log_t + 1][8]: per FORS level the H state after ADRS rounds 0..4
 };
 
 __device__ __forceinline__ uint64_t shr64(uint64_t x, int s) { return s >= 64 ? 0ull : (x >> s); }
@@ -694,7 +695,9 @@ __global__ void __launch_bounds__(kTreeBlock) shared_root_kernel(LaunchArgs a) {
 // ---------------------------------------------------------------------------
 // 768 lanes keep the register budget at 85 per thread (65536 / 768).
 constexpr int kForsMaxLanes = 768;
-constexpr int kForsPrefixWords = 16;  // per-message PRF / F prefix states at the head of smem
+// per-message PRF / F prefix states (16 words) and per-level H prefix states
+// ((log_t + 1) x 8 words, log_t <= 9) at the head of FORS_Sign's smem
+constexpr int kForsPrefixWords = 16 + 8 * 10;
 
 template <int S>
 __host__ __device__ constexpr int fors_smem_words_per_tree(bool relax) {
@@ -794,7 +797,30 @@ __global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) 
   const Adrs fa = make_adrs(0, pl.tree, ADDR_FORS_TREE, pl.leaf, 0, 0);
 
   const int tid = threadIdx.x;
-  if (tid == 0) fors_prefix<S, V>(mid, sks, fa, pre);
+  // Every H of FORS level L of this message has ADRS words 0..4 = (layer 0,
+  // tree, FORS_TREE, keypair, height L, hash index >> 16 = 0): SHA-256 rounds
+  // 0..4 of its first block are computed once per level here (lpre[L]) and by
+  // pass 0 handed to the level grids.
+  static_assert(Pr::k * Pr::t <= 65536, "FORS hash index must fit ADRS bytes 20..21");
+  uint32_t* lpre = sm + 16;
+  if (tid == 0) {
+    fors_prefix<S, V>(mid, sks, fa, pre);
+  } else if (tid <= Pr::log_t) {
+    Adrs la = fa;
+    adrs_set_chain_hash(la, (uint32_t)tid, 0u);
+    const uint32_t W04[5] = {la.w0, la.w1, la.w2, la.w3, la.w4};
+    uint32_t s5[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) s5[i] = mid[i];
+    rounds_prefix<V, 5>(s5, W04);
+#pragma unroll
+    for (int i = 0; i < 8; i++) lpre[tid * 8 + i] = s5[i];
+    if (a.fors_lpre && pass == 0) {
+      uint32_t* g = a.fors_lpre + ((size_t)msg * (Pr::log_t + 1) + tid) * 8;
+#pragma unroll
+      for (int i = 0; i < 8; i++) g[i] = s5[i];
+    }
+  }
   __syncthreads();
 
   // ---- leaf phase (vexec.py:387-435) ----
@@ -838,7 +864,7 @@ __global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) 
       for (int j = 0; j < NW; j++) { m[j] = l0[j]; m[NW + j] = l1[j]; }
       Adrs pa = fa;
       adrs_set_chain_hash(pa, 1, (uint32_t)lane_leaf + ((uint32_t)(g * t) >> 1));
-      thash_reg<V, 2 * NW>(par, mid, pa, m);
+      thash_reg_pre<V, 2 * NW>(par, mid, lpre + 8, pa, m);
       if (to_global) {
         uint32_t* d = a.fors_nodes[0] + (((size_t)msg * Pr::k + g) * (t / 2) + lane_leaf) * NW;
 #pragma unroll
@@ -886,7 +912,7 @@ __global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) 
       uint32_t par[8];
       Adrs na = fa;
       adrs_set_chain_hash(na, (uint32_t)lvl, (uint32_t)j + ((uint32_t)(g * t) >> lvl));
-      thash_reg<V, 2 * NW>(par, mid, na, m);
+      thash_reg_pre<V, 2 * NW>(par, mid, lpre + lvl * 8, na, m);
       if (lvl == Pr::log_t) {
         uint32_t* r = a.fors_roots + ((size_t)msg * Pr::k + g) * 8;
 #pragma unroll
@@ -937,12 +963,13 @@ __global__ void __launch_bounds__(kForsLevelBlock) fors_level_kernel(LaunchArgs 
   constexpr int tree_sig = (1 + Pr::log_t) * Pr::n;
   uint8_t* fsig = a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_fors;
   if ((sel >> 1) == j) store_node<NW>(fsig + g * tree_sig + Pr::n + (L - 1) * Pr::n, (sel & 1u) ? m : m + NW);
-  uint32_t mid[8], par[8];
+  uint32_t mid[8], pre5[8], par[8];
+  const uint32_t* lp = a.fors_lpre + ((size_t)msg * (Pr::log_t + 1) + L) * 8;
 #pragma unroll
-  for (int w = 0; w < 8; w++) mid[w] = K.thash_mid[w];
+  for (int w = 0; w < 8; w++) { mid[w] = K.thash_mid[w]; pre5[w] = lp[w]; }
   Adrs na = make_adrs(0, pl.tree, ADDR_FORS_TREE, pl.leaf, 0, 0);
   adrs_set_chain_hash(na, (uint32_t)L, j + ((g * (uint32_t)t) >> L));
-  thash_reg<V, 2 * NW>(par, mid, na, m);
+  thash_reg_pre<V, 2 * NW>(par, mid, pre5, na, m);
   uint32_t* d = (L == Pr::log_t) ? a.fors_roots + tg * 8 : a.fors_nodes[par_buf] + (tg * per_tree + j) * NW;
 #pragma unroll
   for (int w = 0; w < NW; w++) d[w] = par[w];

@@ -338,6 +338,37 @@ __device__ __forceinline__ void thash_reg(uint32_t st[8], const uint32_t mid[8],
   }
 }
 
+// thash_reg with the first block resumed after round 5: `pre5` is the state
+// after rounds 0..4 from `mid` over ADRS words 0..4, computed once for every
+// hash that shares them (e.g. one FORS level of one message).
+template <class V, int MW>
+__device__ __forceinline__ void thash_reg_pre(uint32_t st[8], const uint32_t mid[8], const uint32_t pre5[8],
+                                              const Adrs& a, const uint32_t* m) {
+  constexpr int total = 22 + 4 * MW;
+  constexpr int nblk = (total + 9 + 63) / 64;
+  constexpr int SW = 16 * nblk;
+  uint32_t s[SW];
+  s[0] = a.w0; s[1] = a.w1; s[2] = a.w2; s[3] = a.w3; s[4] = a.w4;
+  s[5] = join16(a.h5, m[0]);
+#pragma unroll
+  for (int j = 1; j < MW; j++) s[5 + j] = join16(m[j - 1], m[j]);
+  s[5 + MW] = (m[MW - 1] << 16) | 0x8000u;
+#pragma unroll
+  for (int j = 6 + MW; j < SW - 1; j++) s[j] = 0;
+  s[SW - 1] = (uint32_t)((64 + total) * 8);
+  uint32_t sR[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) { st[i] = mid[i]; sR[i] = pre5[i]; }
+#pragma unroll
+  for (int blk = 0; blk < nblk; blk++) {
+    uint32_t W[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) W[j] = s[16 * blk + j];
+    if (blk == 0) compress_resume<V, 5>(st, sR, W);
+    else compress<V>(st, W);
+  }
+}
+
 // WOTS+ chain (wots.py:42-60): `steps` applications of F starting at hash
 // index `start`, x updated in place.  Along a chain only ADRS bytes 20..21
 // (the hash index, < 2^16) and the node change, so message words W0..W4 are

@@ -69,9 +69,10 @@ def test_work_unit_formula(golden, set_id):
 
 def test_fors_smem_accounting(L):
     # ping-pong regions: 1.5 t nodes per tree (0.75 t with relax)
-    # + 64 bytes of per-message SHA-256 prefix states
-    assert hs.Engine.fors_smem_bytes("128f", 11, 3, False) == 33 * 96 * 16 + 64
-    assert hs.Engine.fors_smem_bytes("256f", 2, 2, True) == 4 * 384 * 32 + 64
+    # + 64 bytes of per-message PRF / F prefix states + 10 x 32 bytes of per-level H prefix states
+    head = 64 + 10 * 32
+    assert hs.Engine.fors_smem_bytes("128f", 11, 3, False) == 33 * 96 * 16 + head
+    assert hs.Engine.fors_smem_bytes("256f", 2, 2, True) == 4 * 384 * 32 + head
 
 
 def test_no_device_fails_loudly(L):
