@@ -147,38 +147,50 @@ __global__ void msg_prep_kernel(LaunchArgs a) {
   const uint8_t* msg = a.msgs + a.offs[i];
   const uint64_t mlen = a.offs[i + 1] - a.offs[i];
 
-  // R = HMAC-SHA-256(sk_prf, opt_rand || msg)[:n]
-  ByteSha<V> hs;
-  uint32_t inner[8], R[8];
-  hs.init_mid(K.hmac_i, 64);
-  if (a.opt_rand) hs.bytes(a.opt_rand + (size_t)i * n, n);
-  else hs.words(K.pk_seed, n);
-  hs.bytes(msg, mlen);
-  hs.final(inner);
-  hs.init_mid(K.hmac_o, 64);
-  hs.words(inner, 32);
-  hs.final(R);
+  constexpr int NW = Pr::NW;
+  // R = HMAC-SHA-256(sk_prf, opt_rand || msg)[:n]  (hashes.py:152-165)
+  uint32_t st[8], R[8];
+  {
+    uint32_t pre[NW];
+    const uint8_t* o = a.opt_rand ? a.opt_rand + (size_t)i * n : nullptr;
+#pragma unroll
+    for (int j = 0; j < NW; j++) pre[j] = o ? load_be(o + 4 * j) : K.pk_seed[j];
+#pragma unroll
+    for (int j = 0; j < 8; j++) st[j] = K.hmac_i[j];
+    sha_prefix_msg<V, NW>(st, 64, pre, msg, mlen);
+    uint32_t W[16];
+#pragma unroll
+    for (int j = 0; j < 8; j++) { W[j] = st[j]; R[j] = K.hmac_o[j]; }
+    W[8] = 0x80000000u;
+#pragma unroll
+    for (int j = 9; j < 15; j++) W[j] = 0;
+    W[15] = (64 + 32) * 8;
+    compress<V>(R, W);
+  }
   uint8_t* sig = a.sigs + (size_t)i * Pr::sig_bytes;
-  store_node<Pr::NW>(sig, R);
+  store_node<NW>(sig, R);
 
-  // H_msg: MGF1(R || PK.seed || SHA-256(R || PK.seed || PK.root || M), digest_bytes)
+  // H_msg: MGF1(R || PK.seed || SHA-256(R || PK.seed || PK.root || M), digest_bytes)  (hashes.py:167-191)
   uint32_t dig0[8];
-  hs.init_iv();
-  hs.words(R, n);
-  hs.words(K.pk_seed, n);
-  hs.words(K.pk_root, n);
-  hs.bytes(msg, mlen);
-  hs.final(dig0);
+  {
+    uint32_t pre[3 * NW];
+#pragma unroll
+    for (int j = 0; j < NW; j++) { pre[j] = R[j]; pre[NW + j] = K.pk_seed[j]; pre[2 * NW + j] = K.pk_root[j]; }
+#pragma unroll
+    for (int j = 0; j < 8; j++) dig0[j] = IVc(j);
+    sha_prefix_msg<V, 3 * NW>(dig0, 0, pre, msg, mlen);
+  }
   uint8_t dg[64];
   constexpr int nctr = (Pr::digest_bytes + 31) / 32;
+#pragma unroll 1
   for (int c = 0; c < nctr; c++) {
-    uint32_t o[8];
-    hs.init_iv();
-    hs.words(R, n);
-    hs.words(K.pk_seed, n);
-    hs.words(dig0, 32);
-    hs.word((uint32_t)c);
-    hs.final(o);
+    uint32_t pre[2 * NW + 9], o[8];
+#pragma unroll
+    for (int j = 0; j < NW; j++) { pre[j] = R[j]; pre[NW + j] = K.pk_seed[j]; }
+#pragma unroll
+    for (int j = 0; j < 8; j++) { pre[2 * NW + j] = dig0[j]; o[j] = IVc(j); }
+    pre[2 * NW + 8] = (uint32_t)c;
+    sha_prefix_msg<V, 2 * NW + 9>(o, 0, pre, msg, 0);
     for (int j = 0; j < 32; j++) dg[32 * c + j] = (uint8_t)(o[j >> 2] >> (24 - 8 * (j & 3)));
   }
   uint64_t tree = 0;

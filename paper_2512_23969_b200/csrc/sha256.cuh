@@ -546,6 +546,54 @@ struct TStream {
 };
 
 // ---------------------------------------------------------------------------
+// Word-level SHA-256 over  prefix (P big-endian words, compile-time count) ||
+// M (mlen bytes, arbitrary length and alignment) || padding, starting from
+// state `st` after `absorbed` bytes (a midstate: 64, or 0 from the IV).  Every
+// message-preparation hash has this shape with M word-aligned after the prefix
+// (HMAC inner: opt_rand || M; H_msg: R || PK.seed || PK.root || M), so M is
+// read as whole words and no block buffer is indexed dynamically (the byte
+// streamer below keeps its block in local memory).  hashes.py:152-191.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t msg_word(const uint8_t* m, uint64_t mlen, uint64_t w) {
+  const uint64_t b = 4 * w;
+  if (b + 4 <= mlen) return ((uint32_t)m[b] << 24) | ((uint32_t)m[b + 1] << 16) | ((uint32_t)m[b + 2] << 8) | m[b + 3];
+  if (b > mlen) return 0u;
+  uint32_t v = 0;
+  const int r = (int)(mlen - b);  // 0..3 bytes left, then the 0x80 padding byte
+  for (int i = 0; i < r; i++) v |= (uint32_t)m[b + i] << (24 - 8 * i);
+  return v | (0x80u << (24 - 8 * r));
+}
+
+template <class V, int P>
+__device__ __forceinline__ void sha_prefix_msg(uint32_t st[8], uint64_t absorbed, const uint32_t (&pre)[P > 0 ? P : 1],
+                                               const uint8_t* m, uint64_t mlen) {
+  const uint64_t data = 4ull * P + mlen;                 // bytes hashed here
+  const uint64_t nblk = (data + 9 + 63) / 64;
+  const uint64_t bits = (absorbed + data) * 8;
+  constexpr int PB = (P + 15) / 16;                      // blocks holding prefix words
+#pragma unroll
+  for (int b = 0; b < PB; b++) {
+    if ((uint64_t)b >= nblk) break;
+    uint32_t W[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      const int k = 16 * b + j;
+      W[j] = k < P ? pre[k < P ? k : 0] : msg_word(m, mlen, (uint64_t)(k - P));
+    }
+    if ((uint64_t)b == nblk - 1) { W[14] = (uint32_t)(bits >> 32); W[15] = (uint32_t)bits; }
+    compress<V>(st, W);
+  }
+#pragma unroll 1
+  for (uint64_t b = PB; b < nblk; b++) {
+    uint32_t W[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) W[j] = msg_word(m, mlen, 16 * b + j - P);
+    if (b == nblk - 1) { W[14] = (uint32_t)(bits >> 32); W[15] = (uint32_t)bits; }
+    compress<V>(st, W);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Generic byte-stream SHA-256 (message preparation only: HMAC, H_msg, MGF1).
 // One thread per message; the block buffer is thread-local.
 // ---------------------------------------------------------------------------

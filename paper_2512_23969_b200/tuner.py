@@ -337,7 +337,7 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
     out = PinnedBuffer(count * p.sig_bytes)
     stable = {}
     try:
-        for T in (1, 2, 4):
+        for T in (1, 2, 3, 4, 6, 8):
             engine.set_config(set_id, streams=T)
             engine.sign_into(set_id, blob, offs, count, out.ptr)
             runs = []
