@@ -149,7 +149,7 @@ __global__ void msg_prep_kernel(LaunchArgs a) {
 
   constexpr int NW = Pr::NW;
   // R = HMAC-SHA-256(sk_prf, opt_rand || msg)[:n]  (hashes.py:152-165)
-  uint32_t st[8], R[8];
+  uint32_t st[8], R[8], mw[17];
   {
     uint32_t pre[NW];
     const uint8_t* o = a.opt_rand ? a.opt_rand + (size_t)i * n : nullptr;
@@ -157,7 +157,12 @@ __global__ void msg_prep_kernel(LaunchArgs a) {
     for (int j = 0; j < NW; j++) pre[j] = o ? load_be(o + 4 * j) : K.pk_seed[j];
 #pragma unroll
     for (int j = 0; j < 8; j++) st[j] = K.hmac_i[j];
-    sha_prefix_msg<V, NW>(st, 64, pre, msg, mlen);
+    if (mlen <= kShortMsgBytes) {
+      load_short_msg(msg, mlen, mw);
+      sha_prefix_words<V, NW>(st, 64, pre, mw, mlen);
+    } else {
+      sha_prefix_msg<V, NW>(st, 64, pre, msg, mlen);
+    }
     uint32_t W[16];
 #pragma unroll
     for (int j = 0; j < 8; j++) { W[j] = st[j]; R[j] = K.hmac_o[j]; }
@@ -178,7 +183,8 @@ __global__ void msg_prep_kernel(LaunchArgs a) {
     for (int j = 0; j < NW; j++) { pre[j] = R[j]; pre[NW + j] = K.pk_seed[j]; pre[2 * NW + j] = K.pk_root[j]; }
 #pragma unroll
     for (int j = 0; j < 8; j++) dig0[j] = IVc(j);
-    sha_prefix_msg<V, 3 * NW>(dig0, 0, pre, msg, mlen);
+    if (mlen <= kShortMsgBytes) sha_prefix_words<V, 3 * NW>(dig0, 0, pre, mw, mlen);
+    else sha_prefix_msg<V, 3 * NW>(dig0, 0, pre, msg, mlen);
   }
   uint8_t dg[64];
   constexpr int nctr = (Pr::digest_bytes + 31) / 32;

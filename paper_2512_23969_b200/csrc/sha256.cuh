@@ -593,6 +593,37 @@ __device__ __forceinline__ void sha_prefix_msg(uint32_t st[8], uint64_t absorbed
   }
 }
 
+// Short messages (mlen <= 64): M is loaded once as 17 padded words (all loads
+// issued up front, predicated on mlen) and every hash over prefix || M reads
+// it from registers -- the message-preparation chain is latency bound (one
+// thread per message), so the loads must not sit between compressions.
+constexpr int kShortMsgBytes = 64;
+__device__ __forceinline__ void load_short_msg(const uint8_t* m, uint64_t mlen, uint32_t (&mw)[17]) {
+#pragma unroll
+  for (int j = 0; j < 17; j++) mw[j] = msg_word(m, mlen, (uint64_t)j);
+}
+
+template <class V, int P>
+__device__ __forceinline__ void sha_prefix_words(uint32_t st[8], uint64_t absorbed, const uint32_t (&pre)[P],
+                                                 const uint32_t (&mw)[17], uint64_t mlen) {
+  const uint64_t data = 4ull * P + mlen;
+  const uint32_t nblk = (uint32_t)((data + 9 + 63) / 64);
+  const uint64_t bits = (absorbed + data) * 8;
+  constexpr int NBMAX = (4 * P + kShortMsgBytes + 9 + 63) / 64;
+#pragma unroll
+  for (int b = 0; b < NBMAX; b++) {
+    if ((uint32_t)b >= nblk) break;
+    uint32_t W[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      const int k = 16 * b + j;
+      W[j] = k < P ? pre[k < P ? k : 0] : (k - P < 17 ? mw[k - P < 17 ? k - P : 0] : 0u);
+    }
+    if ((uint32_t)b == nblk - 1) { W[14] = (uint32_t)(bits >> 32); W[15] = (uint32_t)bits; }
+    compress<V>(st, W);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Generic byte-stream SHA-256 (message preparation only: HMAC, H_msg, MGF1).
 // One thread per message; the block buffer is thread-local.
