@@ -179,6 +179,7 @@ struct SetState {
 using GraphKey = std::tuple<int, uint32_t, int, int, uint64_t, std::string>;
 
 constexpr int kMaxStreams = 8;
+constexpr size_t kMaxGraphs = 64;  // captured batch graphs kept per handle
 constexpr size_t kSharedBudgetBytes = (size_t)8 << 30;  // shared-subtree table cap
 
 }  // namespace
@@ -580,6 +581,10 @@ int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nu
                      "/L" + std::to_string(St.shared_eff) + "/T" + std::to_string(T)};
     auto it = h->graphs.find(key);
     if (it == h->graphs.end()) {
+      // bounded cache: a caller that keeps changing batch shapes or configs
+      // (the tuner, a service with many batch sizes) re-captures instead of
+      // accumulating executable graphs
+      if (h->graphs.size() >= kMaxGraphs) drop_graphs(h);
       cudaGraph_t g;
       CUDA_TRY(h, cudaStreamBeginCapture(h->s0, cudaStreamCaptureModeThreadLocal));
       cudaError_t e = enqueue_batch(h, set, count, T, true);
