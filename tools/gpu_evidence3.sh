@@ -2,8 +2,10 @@
 # Final round-1 evidence for the current code: bench (+ reference arm), launch
 # lists per set (graph mode), full ncu captures of the kernels on the path,
 # BASELINE config 5 stress.
-OUT=gpurun_out/ev3; mkdir -p $OUT
+OUT=${EVOUT:-gpurun_out/ev3}; mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/smi.txt
+timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/pytest.txt 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 900 python bench.py --impl reference > $OUT/ref.json 2> $OUT/ref.err
 for s in 128f 192f 256f; do
