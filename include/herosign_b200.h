@@ -74,9 +74,10 @@ typedef struct {
   int32_t shared_layers;      /* top hypertree layers whose subtrees are
                                  computed once per (key, tree) per batch
                                  instead of once per message (0 = off; max
-                                 5 for 128f/192f, 4 for 256f)                */
+                                 6 for 128f/192f, 4 for 256f; only the
+                                 subtrees the batch reads are computed)      */
   int32_t shared_auto;        /* 1: per batch, share a layer only when its
-                                 shareable subtrees are fewer than half the
+                                 subtrees per key are at most twice the key's
                                  messages (and within the table budget);
                                  0: share exactly shared_layers              */
   int32_t fors_cta_levels;    /* FORS tree levels reduced inside FORS_Sign's
@@ -160,7 +161,8 @@ HS_API int64_t hs_launch_count(hs_t *h);
 /* Shape of the staged batch as the engine will run it: out[0] staged
  * messages, out[1] subtree-sharing depth chosen for it (shared_auto policy),
  * out[2] FORS levels kept in the CTA (fors_cta_levels resolved), out[3]
- * tree_split.  Returns the number of values written. */
+ * tree_split, out[4] shared subtrees its last run computed (synchronises the
+ * handle's stream).  Returns the number of values written. */
 HS_API int hs_batch_info(hs_t *h, int set, int32_t *out, int cap);
 
 /* SHA-256 arithmetic paths compiled into this library (hs_set_config.variant

@@ -59,7 +59,7 @@ class TuningConfig:
                         "WOTS_Sign": "tuned" if tuned_all else "baseline"}
             b200 = dict(B200_DEFAULTS[set_id])
             b200.update({"variant": {k: 0 for k in KERNELS}, "wots_from_tree": True, "chunk": 16384, "streams": 1,
-                         "shared_layers": 4 if set_id == "256f" else 5, "shared_auto": True})
+                         "shared_layers": 4 if set_id == "256f" else 6, "shared_auto": True})
             sets[set_id] = SetConfig(best, padding_solve(p.n), backends, set_id == "256f", b200)
         return cls(seme_per_block=seme, sets=sets)
 

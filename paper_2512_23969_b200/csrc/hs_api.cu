@@ -68,6 +68,18 @@ size_t shared_end_words(int set, int layers) {
   return 0;
 }
 
+// shared subtrees per key for `layers` top layers: sum_{j<layers} 2^(hp*j)
+size_t shared_units_of(int set, int layers) {
+  size_t u = 0;
+  for (int j = 0; j < layers; j++) u += (size_t)1 << (kInfo[set].hp * j);
+  return u;
+}
+
+// key_used flags (nkeys) followed by per-key flags of every shared subtree
+size_t used_flag_bytes(int set, uint32_t nkeys, int layers) {
+  return (size_t)nkeys * (1 + shared_units_of(set, layers));
+}
+
 int shared_max(int set) {
   switch (set) {
     case 0: return shared_max_layers<0>();
@@ -361,10 +373,11 @@ LaunchArgs make_args(hs_t* h, int set, uint32_t first, uint32_t count) {
   // subtree sharing needs the stash (WOTS gather) and a table sized for the key set
   const int L = St.shared_eff;
   if (a.stash && L > 0 && B.shared && B.shared_cap >= (size_t)St.nkeys * shared_words(set, L) && B.key_used &&
-      B.key_used_cap >= St.nkeys) {
+      B.key_used_cap >= used_flag_bytes(set, St.nkeys, L)) {
     a.shared = B.shared;
     a.shared_layers = L;
     a.key_used = B.key_used;
+    a.unit_used = B.key_used + St.nkeys;
     if (St.cfg.tree_split && B.sends && B.sends_cap >= (size_t)St.nkeys * shared_end_words(set, L))
       a.shared_ends = B.sends;
   }
@@ -441,7 +454,8 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
 #define TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
   int kernels = 2;  // msg_prep + WOTS; the shared / FORS / TREE branches are counted by enqueue_*
   TRY(rec(0, h->s0));
-  if (a.shared_layers > 0) TRY(cudaMemsetAsync(a.key_used, 0, a.nkeys, h->s0));
+  if (a.shared_layers > 0)
+    TRY(cudaMemsetAsync(a.key_used, 0, used_flag_bytes(set, a.nkeys, a.shared_layers), h->s0));
   TRY(launch(set, K_PREP, c.variant[3], a, h->s0));
   TRY(rec(1, h->s0));
   if (serial) {
@@ -520,7 +534,8 @@ cudaError_t enqueue_batch(hs_t* h, int set, uint32_t count, int T, bool capture)
   int kernels = 0;
 #define TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
   TRY(rec(h->ev[0], h->s0));
-  if (all.shared_layers > 0) TRY(cudaMemsetAsync(all.key_used, 0, all.nkeys, h->s0));
+  if (all.shared_layers > 0)
+    TRY(cudaMemsetAsync(all.key_used, 0, used_flag_bytes(set, all.nkeys, all.shared_layers), h->s0));
   TRY(launch(set, K_PREP, c.variant[3], all, h->s0));
   kernels++;
   TRY(rec(h->ev[1], h->s0));
@@ -652,8 +667,11 @@ int stage_inputs(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, co
     CUDA_TRY(h, cudaMemcpyAsync(B.optrand, opt_rand + (size_t)first * I.n, (size_t)count * I.n,
                                 cudaMemcpyHostToDevice, h->s0));
   // Subtree sharing depth for this batch: at most cfg.shared_layers, within
-  // the table budget, and (auto policy) only layers whose shareable subtrees
-  // are clearly fewer than the messages that would otherwise recompute them.
+  // the table budget, and (auto policy) only layers with at most twice as many
+  // subtrees per key as the key's messages.  Only subtrees some message reads
+  // are computed (msg_prep flags them), so with c messages over U subtrees a
+  // shared layer costs U(1 - e^(-c/U)) subtrees instead of c: <= 0.79 c at
+  // U = 2c, 0.63 c at U = c.
   St.shared_eff = 0;
   if (St.cfg.shared_layers > 0 && St.cfg.wots_from_tree) {
     uint32_t used = 1;
@@ -667,7 +685,7 @@ int stage_inputs(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, co
     int L = 0;
     while (L < St.cfg.shared_layers) {
       const size_t units_j = (size_t)1 << (hp * L);  // subtrees at depth L per key
-      if (St.cfg.shared_auto && units_j * used * 2 > count) break;
+      if (St.cfg.shared_auto && units_j * used > 2 * (size_t)count) break;
       if ((size_t)St.nkeys * shared_words(set, L + 1) * 4 > kSharedBudgetBytes) break;
       L++;
     }
@@ -677,7 +695,7 @@ int stage_inputs(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, co
     const size_t need = (size_t)St.nkeys * shared_words(set, St.shared_eff);
     void* before[3] = {B.shared, B.key_used, B.sends};
     CUDA_TRY(h, grow(B.shared, B.shared_cap, need));
-    CUDA_TRY(h, grow(B.key_used, B.key_used_cap, (size_t)St.nkeys));
+    CUDA_TRY(h, grow(B.key_used, B.key_used_cap, used_flag_bytes(set, St.nkeys, St.shared_eff)));
     if (St.cfg.tree_split)
       CUDA_TRY(h, grow(B.sends, B.sends_cap, (size_t)St.nkeys * shared_end_words(set, St.shared_eff)));
     void* after[3] = {B.shared, B.key_used, B.sends};
@@ -1053,8 +1071,18 @@ int64_t hs_launch_count(hs_t* h) { return h ? h->launches : -1; }
 int hs_batch_info(hs_t* h, int set, int32_t* out, int cap) {
   if (!h || !valid_set(set) || (cap > 0 && !out)) return fail(h, HS_E_USAGE, "bad arguments");
   const SetState& St = h->sets[set];
-  const int32_t v[4] = {(int32_t)St.staged, St.shared_eff, fors_cta_levels(set, St.cfg), St.cfg.tree_split};
-  const int n = std::min(cap, 4);
+  // shared subtrees the last run of the staged batch computed (flags set by msg_prep)
+  int32_t built = 0;
+  const Buffers& B = h->buf[set];
+  if (cap > 4 && St.shared_eff > 0 && B.key_used && B.key_used_cap >= used_flag_bytes(set, St.nkeys, St.shared_eff)) {
+    std::vector<uint8_t> f((size_t)St.nkeys * shared_units_of(set, St.shared_eff));
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    CUDA_TRY(h, cudaStreamSynchronize(h->s0));
+    CUDA_TRY(h, cudaMemcpy(f.data(), B.key_used + St.nkeys, f.size(), cudaMemcpyDeviceToHost));
+    for (uint8_t x : f) built += x != 0;
+  }
+  const int32_t v[5] = {(int32_t)St.staged, St.shared_eff, fors_cta_levels(set, St.cfg), St.cfg.tree_split, built};
+  const int n = std::min(cap, 5);
   for (int i = 0; i < n; i++) out[i] = v[i];
   return n;
 }

@@ -66,6 +66,7 @@ struct LaunchArgs {
   uint32_t* shared;          // nkeys * units * shared_rec_words(S) (nullable)
   int shared_layers;         // 0 = off
   uint8_t* key_used;         // nkeys flags set by msg_prep
+  uint8_t* unit_used;        // nkeys x units(shared_layers) flags set by msg_prep: shared subtrees the batch reads
   const uint8_t* pks;        // verify: nkeys * 2n (pk_seed || pk_root)
   const uint8_t* vsigs;      // verify: count * sig_bytes
   uint8_t* ok;               // verify: count flags
@@ -131,6 +132,26 @@ __global__ void key_setup_kernel(LaunchArgs a) {
   for (int j = 0; j < 8; j++) kd.prf_mid[j] = IVc(j);
   rounds_prefix<V, Pr::NW>(kd.prf_mid, kd.sk_seed);
   a.keys_out[i] = kd;
+}
+
+// layer schedule (sigcore.py:107-121)
+template <int S>
+__device__ __forceinline__ void layer_coords(const MsgPlan& pl, int layer, uint64_t& tree, uint32_t& leaf) {
+  using Pr = P<S>;
+  if (layer == 0) {
+    tree = pl.tree;
+    leaf = pl.leaf;
+  } else {
+    leaf = (uint32_t)(shr64(pl.tree, Pr::hp * (layer - 1)) & (uint64_t)(Pr::leaves - 1));
+    tree = shr64(pl.tree, Pr::hp * layer);
+  }
+}
+
+// Shared subtrees per key for L shared top layers: sum_{j<L} 2^(hp*j) (layer
+// d-1-j holds 2^(hp*j) trees); unit u of depth j is units(j) + tree.
+template <int S>
+__host__ __device__ constexpr int shared_units(int L) {
+  return L <= 0 ? 0 : shared_units<S>(L - 1) + (1 << (P<S>::hp * (L - 1)));
 }
 
 // ---------------------------------------------------------------------------
@@ -211,6 +232,15 @@ __global__ void msg_prep_kernel(LaunchArgs a) {
   pl.key = key;
   a.plans[i] = pl;
   if (a.key_used) a.key_used[key] = 1;
+  if (a.unit_used) {  // the shared subtrees this message's top layers read
+    const int U = shared_units<S>(a.shared_layers);
+    for (int j = 0; j < a.shared_layers; j++) {
+      uint64_t t;
+      uint32_t lf;
+      layer_coords<S>(pl, Pr::d - 1 - j, t, lf);
+      a.unit_used[(size_t)key * U + shared_units<S>(j) + (uint32_t)t] = 1;
+    }
+  }
   // FORS indices, LSB-first bit order within each byte (sigcore.py:75-90)
   int off = 0;
   for (int g = 0; g < Pr::k; g++) {
@@ -220,18 +250,6 @@ __global__ void msg_prep_kernel(LaunchArgs a) {
   }
 }
 
-// layer schedule (sigcore.py:107-121)
-template <int S>
-__device__ __forceinline__ void layer_coords(const MsgPlan& pl, int layer, uint64_t& tree, uint32_t& leaf) {
-  using Pr = P<S>;
-  if (layer == 0) {
-    tree = pl.tree;
-    leaf = pl.leaf;
-  } else {
-    leaf = (uint32_t)(shr64(pl.tree, Pr::hp * (layer - 1)) & (uint64_t)(Pr::leaves - 1));
-    tree = shr64(pl.tree, Pr::hp * layer);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // One WOTS+ leaf (wots.py:119-143): wots_len chains of PRF + (w-1) F, then
@@ -527,14 +545,15 @@ __global__ void __launch_bounds__(kTreeBlock) tree_root_kernel(LaunchArgs a) {
 template <int S>
 struct Shared {
   using Pr = P<S>;
-  // one layer deeper than the 2^(hp*j) units reach ~4096 per key: the auto
-  // policy shares it only for batches of >= 8192 messages per key
-  static constexpr int max_layers = Pr::hp >= 4 ? 4 : 5;
+  // down to the layer with 2^(hp*j) = 32768 (hp 3) / 4096 (hp 4) subtrees per
+  // key; the auto policy shares a layer only when its subtrees are at most
+  // twice the key's messages (and only the subtrees the batch reads are built)
+  static constexpr int max_layers = Pr::hp >= 4 ? 4 : 6;
   static constexpr int node_words = (2 * Pr::leaves - 1) * 8;
   static constexpr int leaf_stash_words = Pr::wots_len * Pr::w * Pr::NW;
   static constexpr int rec_words = node_words + Pr::leaves * leaf_stash_words;
   // units per key for L shared layers: sum_{j<L} 2^(hp*j)
-  __host__ __device__ static constexpr int units(int L) { return L <= 0 ? 0 : units(L - 1) + (1 << (Pr::hp * (L - 1))); }
+  __host__ __device__ static constexpr int units(int L) { return shared_units<S>(L); }
   // level offset (in nodes) inside a record
   __device__ static constexpr int level_off(int lvl) { return lvl == 0 ? 0 : level_off(lvl - 1) + (Pr::leaves >> (lvl - 1)); }
   // record of (key, layer, tree); layer >= d - L
@@ -555,7 +574,8 @@ __global__ void __launch_bounds__(kTreeBlock, (S == 2 ? kTreeMinBlocks8 : kTreeM
   const uint64_t per_key = (uint64_t)U * Pr::leaves;
   const uint64_t gid = (uint64_t)blockIdx.x * kTreeBlock + threadIdx.x;
   const uint32_t key = (uint32_t)(gid / per_key);
-  const bool valid = key < a.nkeys && a.key_used[key];
+  const bool valid = key < a.nkeys && a.key_used[key] &&
+                     (!a.unit_used || a.unit_used[(size_t)key * U + (uint32_t)((gid % per_key) / Pr::leaves)]);
   const uint32_t rem = (uint32_t)(gid % per_key);
   const uint32_t unit = rem / Pr::leaves;
   const uint32_t leaf = rem % Pr::leaves;
@@ -612,6 +632,7 @@ __device__ __forceinline__ bool shared_coords(const LaunchArgs& a, uint64_t lid,
   const uint32_t rem = (uint32_t)(lid % per_key);
   const uint32_t unit = rem / Pr::leaves;
   leaf = rem % Pr::leaves;
+  if (a.unit_used && !a.unit_used[(size_t)key * Sh::units(a.shared_layers) + unit]) return false;
   int j = 0;
   while (j + 1 < a.shared_layers && (uint32_t)Sh::units(j + 1) <= unit) j++;
   layer = Pr::d - 1 - j;

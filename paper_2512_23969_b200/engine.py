@@ -260,13 +260,14 @@ class Engine:
 
     def batch_info(self, set_id: str) -> dict:
         """How the staged batch runs: messages, subtree-sharing depth chosen by the
-        auto policy, FORS levels kept in the CTA, split TREE_Sign."""
-        v = (ctypes.c_int32 * 4)()
-        n = _lib.lib().hs_batch_info(self._h, SET_INDEX[set_id], v, 4)
+        auto policy, FORS levels kept in the CTA, split TREE_Sign, and the shared
+        subtrees its last run computed."""
+        v = (ctypes.c_int32 * 5)()
+        n = _lib.lib().hs_batch_info(self._h, SET_INDEX[set_id], v, 5)
         if n < 0:
             self._check(n, "hs_batch_info")
         return {"staged": int(v[0]), "shared_layers": int(v[1]), "fors_cta_levels": int(v[2]),
-                "tree_split": bool(v[3])}
+                "tree_split": bool(v[3]), "shared_subtrees_built": int(v[4])}
 
     def launch_stats(self, reset: bool = True) -> dict:
         """Host-side batch launch latency: cudaGraphLaunch calls since the last reset."""

@@ -275,7 +275,7 @@ def test_subtree_sharing(eng, oracle_mod, set_id):
     ref, _ = oracle_mod.sign_many(set_id, b"".join(sks), kidx, msgs)
     eng.upload_keys(set_id, sks)
     base = eng.config(set_id)
-    top = 4 if set_id == "256f" else 5
+    top = 4 if set_id == "256f" else 6
     try:
         for L in range(top + 1):
             eng.set_config(set_id, shared_layers=L, shared_auto=False)
