@@ -168,6 +168,13 @@ struct Buffers {
   uint32_t* ends = nullptr; size_t ends_cap = 0;  // split TREE_Sign chain ends
   uint32_t* sends = nullptr; size_t sends_cap = 0;  // split shared-subtree chain ends
   uint32_t* lpre = nullptr; size_t lpre_cap = 0;    // per-message, per-FORS-level H prefix states
+  // verification inputs (hs_verify_batch), kept across calls
+  uint8_t* v_pks = nullptr; size_t v_pks_cap = 0;
+  uint8_t* v_msgs = nullptr; size_t v_msgs_cap = 0;
+  uint8_t* v_sigs = nullptr; size_t v_sigs_cap = 0;
+  uint8_t* v_ok = nullptr; size_t v_ok_cap = 0;
+  uint64_t* v_offs = nullptr; size_t v_offs_cap = 0;
+  uint32_t* v_kidx = nullptr; size_t v_kidx_cap = 0;
   // pinned staging
   uint8_t* h_msgs = nullptr; size_t h_msgs_cap = 0;
   uint64_t* h_offs = nullptr; size_t h_offs_cap = 0;
@@ -782,6 +789,8 @@ void hs_close(hs_t* h) {
     cudaFree(B.ends);
     cudaFree(B.sends);
     cudaFree(B.lpre);
+    cudaFree(B.v_pks); cudaFree(B.v_msgs); cudaFree(B.v_sigs); cudaFree(B.v_ok); cudaFree(B.v_offs);
+    cudaFree(B.v_kidx);
     cudaFree(h->sets[s].sk_raw);
   }
   if (h->flush) cudaFree(h->flush);
@@ -980,37 +989,36 @@ int hs_verify_batch(hs_t* h, int set, const uint8_t* pks, uint32_t nkeys, const 
   const uint64_t base = offs[0], mbytes = offs[count] - offs[0];
   std::vector<uint64_t> ro(count + 1);
   for (uint32_t i = 0; i <= count; i++) ro[i] = offs[i] - base;
-  uint8_t *d_pks = nullptr, *d_msgs = nullptr, *d_sigs = nullptr, *d_ok = nullptr;
-  uint64_t* d_offs = nullptr;
-  uint32_t* d_kidx = nullptr;
-  cudaError_t e = cudaMalloc(&d_pks, (size_t)nkeys * 2 * I.n);
-  if (e == cudaSuccess) e = cudaMalloc(&d_msgs, std::max<size_t>(mbytes, 1));
-  if (e == cudaSuccess) e = cudaMalloc(&d_sigs, (size_t)count * I.sig_bytes);
-  if (e == cudaSuccess) e = cudaMalloc(&d_ok, count);
-  if (e == cudaSuccess) e = cudaMalloc(&d_offs, ((size_t)count + 1) * 8);
-  if (e == cudaSuccess && key_idx) e = cudaMalloc(&d_kidx, (size_t)count * 4);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_pks, pks, (size_t)nkeys * 2 * I.n, cudaMemcpyHostToDevice, h->s0);
-  if (e == cudaSuccess && mbytes) e = cudaMemcpyAsync(d_msgs, msgs + base, mbytes, cudaMemcpyHostToDevice, h->s0);
+  // device buffers persist across calls (grown on demand); pinned host inputs
+  // (e.g. the signatures a pinned hs_sign_batch call just wrote) copy async
+  Buffers& B = h->buf[set];
+  cudaError_t e = grow(B.v_pks, B.v_pks_cap, (size_t)nkeys * 2 * I.n);
+  if (e == cudaSuccess) e = grow(B.v_msgs, B.v_msgs_cap, std::max<size_t>(mbytes, 1));
+  if (e == cudaSuccess) e = grow(B.v_sigs, B.v_sigs_cap, (size_t)count * I.sig_bytes);
+  if (e == cudaSuccess) e = grow(B.v_ok, B.v_ok_cap, (size_t)count);
+  if (e == cudaSuccess) e = grow(B.v_offs, B.v_offs_cap, (size_t)count + 1);
+  if (e == cudaSuccess && key_idx) e = grow(B.v_kidx, B.v_kidx_cap, (size_t)count);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(B.v_pks, pks, (size_t)nkeys * 2 * I.n, cudaMemcpyHostToDevice, h->s0);
+  if (e == cudaSuccess && mbytes) e = cudaMemcpyAsync(B.v_msgs, msgs + base, mbytes, cudaMemcpyHostToDevice, h->s0);
   if (e == cudaSuccess)
-    e = cudaMemcpyAsync(d_sigs, sigs, (size_t)count * I.sig_bytes, cudaMemcpyHostToDevice, h->s0);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_offs, ro.data(), ro.size() * 8, cudaMemcpyHostToDevice, h->s0);
+    e = cudaMemcpyAsync(B.v_sigs, sigs, (size_t)count * I.sig_bytes, cudaMemcpyHostToDevice, h->s0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(B.v_offs, ro.data(), ro.size() * 8, cudaMemcpyHostToDevice, h->s0);
   if (e == cudaSuccess && key_idx)
-    e = cudaMemcpyAsync(d_kidx, key_idx, (size_t)count * 4, cudaMemcpyHostToDevice, h->s0);
+    e = cudaMemcpyAsync(B.v_kidx, key_idx, (size_t)count * 4, cudaMemcpyHostToDevice, h->s0);
   LaunchArgs a;
   std::memset(&a, 0, sizeof a);
-  a.pks = d_pks;
+  a.pks = B.v_pks;
   a.nkeys = nkeys;
-  a.msgs = d_msgs;
-  a.offs = d_offs;
-  a.key_idx = d_kidx;
-  a.vsigs = d_sigs;
-  a.ok = d_ok;
+  a.msgs = B.v_msgs;
+  a.offs = B.v_offs;
+  a.key_idx = key_idx ? B.v_kidx : nullptr;
+  a.vsigs = B.v_sigs;
+  a.ok = B.v_ok;
   a.count = count;
   if (e == cudaSuccess) e = launch(set, K_VERIFY, h->sets[set].cfg.variant[2], a, h->s0);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(ok, d_ok, count, cudaMemcpyDeviceToHost, h->s0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(ok, B.v_ok, count, cudaMemcpyDeviceToHost, h->s0);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->s0);
   h->launches++;
-  cudaFree(d_pks); cudaFree(d_msgs); cudaFree(d_sigs); cudaFree(d_ok); cudaFree(d_offs); cudaFree(d_kidx);
   if (e != cudaSuccess) return fail(h, HS_E_CUDA, "verify: %s", cudaGetErrorString(e));
   return HS_OK;
 }

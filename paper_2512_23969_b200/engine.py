@@ -224,6 +224,23 @@ class Engine:
                         "hs_verify_batch")
         return [bool(o) and g for o, g in zip(ok.tolist(), good)]
 
+    def verify_into(self, set_id: str, pks: bytes, blob, offs: np.ndarray, count: int, sigs,
+                    key_idx: np.ndarray | None = None) -> np.ndarray:
+        """Zero-copy batch verify: messages as (blob, offs) and signatures as one
+        buffer of count * sig_bytes (bytes, or a pointer such as the pinned buffer
+        sign_into just filled).  Returns a bool array."""
+        p = derive(set_id)
+        if not pks or len(pks) % p.pk_bytes:
+            raise UsageError(f"public keys must be a multiple of {p.pk_bytes} bytes")
+        ok = np.zeros(count, dtype=np.uint8)
+        kidx = None if key_idx is None else np.ascontiguousarray(key_idx, dtype=np.uint32)
+        with self._lock:
+            self._check(_lib.lib().hs_verify_batch(self._h, p.index, _u8ptr(bytes(pks)), len(pks) // p.pk_bytes,
+                                                   _u8ptr(blob), _u8ptr(offs), _u8ptr(kidx), _u8ptr(sigs),
+                                                   count, _u8ptr(ok)),
+                        "hs_verify_batch")
+        return ok.astype(bool)
+
     # -- device-resident stages (bench / graph signer) ---------------------
     def stage(self, set_id: str, blob, offs: np.ndarray, count: int, key_idx=None, opt_rand=None) -> None:
         p = derive(set_id)

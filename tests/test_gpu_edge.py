@@ -87,3 +87,29 @@ def test_chunked_multistream_mixed_keys(eng, oracle_mod, set_id):
     ref, _ = oracle_mod.sign_many(set_id, b"".join(sks), kidx, msgs, blob)
     bad = [i for i in range(count) if sigs[i] != ref[i]]
     assert not bad, bad[:10]
+
+
+def test_verify_into_pinned_roundtrip(eng, oracle_mod):
+    """verify_into reads the pinned buffer sign_into filled; a flipped byte fails only its message."""
+    import numpy as np
+
+    from paper_2512_23969_b200.engine import PinnedBuffer, pack_messages
+
+    set_id = "128f"
+    p = derive(set_id)
+    rng = random.Random(808)
+    sk = oracle_mod.keygen(set_id, rng.randbytes(3 * p.n))
+    eng.upload_keys(set_id, sk)
+    msgs = [rng.randbytes(rng.choice([0, 32, 90])) for _ in range(300)]
+    blob, offs = pack_messages(msgs)
+    out = PinnedBuffer(len(msgs) * p.sig_bytes)
+    try:
+        eng.sign_into(set_id, blob, offs, len(msgs), out.ptr)
+        assert eng.verify_into(set_id, sk[2 * p.n:], blob, offs, len(msgs), out.ptr).all()
+        out.array()[17 * p.sig_bytes + 1234] ^= 0x40
+        ok = eng.verify_into(set_id, sk[2 * p.n:], blob, offs, len(msgs), out.ptr)
+        assert not ok[17] and ok.sum() == len(msgs) - 1
+        raw = bytes(out.view[: 3 * p.sig_bytes])
+        assert raw[:p.sig_bytes] == oracle_mod.sign(set_id, sk, msgs[0])
+    finally:
+        out.free()
