@@ -1263,23 +1263,20 @@ __global__ void __launch_bounds__(32 * kVerifyWarps) verify_kernel(LaunchArgs a)
     for (int j = 0; j < 8; j++) R[j] = j < NW ? load_be(sig + 4 * j) : 0u;
     const uint8_t* msg = a.msgs + a.offs[i];
     const uint64_t mlen = a.offs[i + 1] - a.offs[i];
-    ByteSha<V> hsh;
-    hsh.init_iv();
-    hsh.words(R, Pr::n);
-    hsh.words(pk_seed, Pr::n);
-    hsh.words(pk_root, Pr::n);
-    hsh.bytes(msg, mlen);
-    hsh.final(dig0);
+    {  // word-level, as msg_prep (sha_prefix_msg)
+      uint32_t pre[3 * NW];
+      for (int j = 0; j < NW; j++) { pre[j] = R[j]; pre[NW + j] = pk_seed[j]; pre[2 * NW + j] = pk_root[j]; }
+      for (int j = 0; j < 8; j++) dig0[j] = IVc(j);
+      sha_prefix_msg<V, 3 * NW>(dig0, 0, pre, msg, mlen);
+    }
     uint8_t dg[64];
     constexpr int nctr = (Pr::digest_bytes + 31) / 32;
     for (int c = 0; c < nctr; c++) {
-      uint32_t o[8];
-      hsh.init_iv();
-      hsh.words(R, Pr::n);
-      hsh.words(pk_seed, Pr::n);
-      hsh.words(dig0, 32);
-      hsh.word((uint32_t)c);
-      hsh.final(o);
+      uint32_t pre[2 * NW + 9], o[8];
+      for (int j = 0; j < NW; j++) { pre[j] = R[j]; pre[NW + j] = pk_seed[j]; }
+      for (int j = 0; j < 8; j++) { pre[2 * NW + j] = dig0[j]; o[j] = IVc(j); }
+      pre[2 * NW + 8] = (uint32_t)c;
+      sha_prefix_msg<V, 2 * NW + 9>(o, 0, pre, msg, 0);
       for (int j = 0; j < 32; j++) dg[32 * c + j] = (uint8_t)(o[j >> 2] >> (24 - 8 * (j & 3)));
     }
     uint64_t tree = 0;

@@ -551,8 +551,8 @@ struct TStream {
 // state `st` after `absorbed` bytes (a midstate: 64, or 0 from the IV).  Every
 // message-preparation hash has this shape with M word-aligned after the prefix
 // (HMAC inner: opt_rand || M; H_msg: R || PK.seed || PK.root || M), so M is
-// read as whole words and no block buffer is indexed dynamically (the byte
-// streamer below keeps its block in local memory).  hashes.py:152-191.
+// read as whole words and no block buffer is indexed dynamically (a byte
+// streamer would keep its block in local memory).  hashes.py:152-191.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t msg_word(const uint8_t* m, uint64_t mlen, uint64_t w) {
   const uint64_t b = 4 * w;
@@ -623,56 +623,5 @@ __device__ __forceinline__ void sha_prefix_words(uint32_t st[8], uint64_t absorb
     compress<V>(st, W);
   }
 }
-
-// ---------------------------------------------------------------------------
-// Generic byte-stream SHA-256 (message preparation only: HMAC, H_msg, MGF1).
-// One thread per message; the block buffer is thread-local.
-// ---------------------------------------------------------------------------
-template <class V>
-struct ByteSha {
-  uint32_t st[8];
-  uint32_t blk[16];
-  uint32_t fill;    // bytes in blk
-  uint64_t total;   // bytes absorbed, including any midstate blocks
-
-  __device__ void init_iv() {
-    for (int i = 0; i < 8; i++) st[i] = IVc(i);
-    fill = 0; total = 0;
-  }
-  __device__ void init_mid(const uint32_t mid[8], uint64_t absorbed) {
-    for (int i = 0; i < 8; i++) st[i] = mid[i];
-    fill = 0; total = absorbed;
-  }
-  __device__ void byte(uint32_t b) {
-    int wi = fill >> 2, sh = 24 - 8 * (fill & 3);
-    if ((fill & 3) == 0) blk[wi] = 0;
-    blk[wi] |= (b & 0xFFu) << sh;
-    fill++;
-    total++;
-    if (fill == 64) {
-      uint32_t W[16];
-      for (int j = 0; j < 16; j++) W[j] = blk[j];
-      compress<V>(st, W);
-      fill = 0;
-    }
-  }
-  __device__ void bytes(const uint8_t* p, uint64_t len) {
-    for (uint64_t i = 0; i < len; i++) byte(p[i]);
-  }
-  __device__ void word(uint32_t w) {  // 4 big-endian bytes
-    byte(w >> 24); byte(w >> 16); byte(w >> 8); byte(w);
-  }
-  __device__ void words(const uint32_t* w, int nbytes) {  // first nbytes of BE words
-    for (int i = 0; i < nbytes; i++) byte(w[i >> 2] >> (24 - 8 * (i & 3)));
-  }
-  __device__ void final(uint32_t out[8]) {
-    uint64_t bits = total * 8;
-    byte(0x80);
-    while (fill != 56) byte(0);
-    word((uint32_t)(bits >> 32));
-    word((uint32_t)bits);
-    for (int i = 0; i < 8; i++) out[i] = st[i];
-  }
-};
 
 }  // namespace hs
