@@ -1359,4 +1359,158 @@ __global__ void __launch_bounds__(32 * kVerifyWarps) verify_kernel(LaunchArgs a)
   }
 }
 
+// ---------------------------------------------------------------------------
+// verify_thread_kernel: one thread per signature (sigcore.py:181-221).  The
+// warp-per-message kernel above leaves 31 lanes idle through every T_len and
+// auth walk and runs 35-67 chains of unequal length on 32 lanes; here each
+// thread walks its own signature and the wots_len chains of a layer as ONE
+// flattened loop of F steps (sum of 15 - digit over the chains, nearly the
+// same count for every thread), pushing each chain end into its T_len stream
+// as the chain completes -- so lanes stay busy and no chain ends are stored.
+// ---------------------------------------------------------------------------
+constexpr int kVerifyThreads = 128;
+
+template <int S, class V>
+__global__ void __launch_bounds__(kVerifyThreads) verify_thread_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  constexpr int NW = Pr::NW;
+  __shared__ uint32_t col[32 * kVerifyThreads];  // per-thread T stream ring (word-interleaved)
+  const uint32_t i = blockIdx.x * kVerifyThreads + threadIdx.x;
+  if (i >= a.count) return;
+  uint32_t* mycol = col + threadIdx.x;
+  const uint32_t key = a.key_idx ? a.key_idx[i] : 0u;
+  const uint8_t* pk = a.pks + (size_t)key * 2 * Pr::n;
+  const uint8_t* sig = a.vsigs + (size_t)i * Pr::sig_bytes;
+  uint32_t pk_seed[8], pk_root[8], mid[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    pk_seed[j] = j < NW ? load_be(pk + 4 * j) : 0u;
+    pk_root[j] = j < NW ? load_be(pk + Pr::n + 4 * j) : 0u;
+  }
+  {
+    uint32_t W[16];
+#pragma unroll
+    for (int j = 0; j < 8; j++) mid[j] = IVc(j);
+#pragma unroll
+    for (int j = 0; j < 16; j++) W[j] = j < NW ? pk_seed[j] : 0u;
+    compress<V>(mid, W);
+  }
+  // H_msg with R = sig[0:n] (hashes.py:175-191), word-level as msg_prep
+  uint32_t R[8], dig0[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) R[j] = j < NW ? load_be(sig + 4 * j) : 0u;
+  const uint8_t* msg = a.msgs + a.offs[i];
+  const uint64_t mlen = a.offs[i + 1] - a.offs[i];
+  {
+    uint32_t pre[3 * NW];
+#pragma unroll
+    for (int j = 0; j < NW; j++) { pre[j] = R[j]; pre[NW + j] = pk_seed[j]; pre[2 * NW + j] = pk_root[j]; }
+#pragma unroll
+    for (int j = 0; j < 8; j++) dig0[j] = IVc(j);
+    sha_prefix_msg<V, 3 * NW>(dig0, 0, pre, msg, mlen);
+  }
+  uint8_t dg[64];
+  constexpr int nctr = (Pr::digest_bytes + 31) / 32;
+#pragma unroll 1
+  for (int c = 0; c < nctr; c++) {
+    uint32_t pre[2 * NW + 9], o[8];
+#pragma unroll
+    for (int j = 0; j < NW; j++) { pre[j] = R[j]; pre[NW + j] = pk_seed[j]; }
+#pragma unroll
+    for (int j = 0; j < 8; j++) { pre[2 * NW + j] = dig0[j]; o[j] = IVc(j); }
+    pre[2 * NW + 8] = (uint32_t)c;
+    sha_prefix_msg<V, 2 * NW + 9>(o, 0, pre, msg, 0);
+    for (int j = 0; j < 32; j++) dg[32 * c + j] = (uint8_t)(o[j >> 2] >> (24 - 8 * (j & 3)));
+  }
+  uint64_t tree = 0;
+  for (int j = 0; j < Pr::tree_bytes; j++) tree = (tree << 8) | dg[Pr::fors_msg_bytes + j];
+  if (Pr::tree_bits < 64) tree &= (1ull << (Pr::tree_bits < 64 ? Pr::tree_bits : 63)) - 1ull;
+  uint32_t leaf_idx = 0;
+  for (int j = 0; j < Pr::leaf_bytes; j++) leaf_idx = (leaf_idx << 8) | dg[Pr::fors_msg_bytes + Pr::tree_bytes + j];
+  leaf_idx &= (1u << Pr::leaf_bits) - 1u;
+
+  // FORS public key (oracle.py:113-146 in reverse): k roots streamed into T_k
+  uint32_t root[8];
+  {
+    const uint8_t* fsig = sig + Pr::off_fors;
+    constexpr int tree_sig = (1 + Pr::log_t) * Pr::n;
+    TStream<V> ts;
+    ts.begin(mid, make_adrs(0, tree, ADDR_FORS_ROOTS, leaf_idx, 0, 0), mycol, kVerifyThreads);
+    int off = 0;
+#pragma unroll 1
+    for (int g = 0; g < Pr::k; g++) {
+      uint32_t sel = 0;
+      for (int j = 0; j < Pr::log_t; j++, off++) sel |= (uint32_t)((dg[off >> 3] >> (off & 7)) & 1) << j;
+      const Adrs fa = make_adrs(0, tree, ADDR_FORS_TREE, leaf_idx, 0, (uint32_t)(g * Pr::t) + sel);
+      uint32_t sk[NW], node[8];
+      load_node<S>(fsig + g * tree_sig, sk);
+      thash_reg<V, NW>(node, mid, fa, sk);
+      walk_auth<S, V>(node, mid, fa, sel, (uint32_t)(g * Pr::t), fsig + g * tree_sig + Pr::n, Pr::log_t);
+      ts.template push_node<NW>(node);
+    }
+    ts.finish(22u + (uint32_t)(Pr::k * Pr::n));
+#pragma unroll
+    for (int j = 0; j < 8; j++) root[j] = ts.st[j];
+  }
+
+  // hypertree: per layer, the wots_len chains as one flattened loop of F steps
+  const uint8_t* ht = sig + Pr::off_ht;
+#pragma unroll 1
+  for (int layer = 0; layer < Pr::d; layer++) {
+    const uint8_t* wsig = ht + (size_t)layer * Pr::layer_bytes;
+    TStream<V> ts;
+    ts.begin(mid, make_adrs((uint32_t)layer, tree, ADDR_WOTS_PK, leaf_idx, 0, 0), mycol, kVerifyThreads);
+    Adrs wa = make_adrs((uint32_t)layer, tree, ADDR_WOTS, leaf_idx, 0, 0);
+    uint32_t x[NW], pre5[8];
+    int c = -1;
+    uint32_t s = Pr::w - 1;  // current hash index; == w-1 means "chain done"
+#pragma unroll 1
+    while (true) {
+      // finish completed chains (a digit of 15 gives a zero-length chain)
+      while (s == (uint32_t)(Pr::w - 1)) {
+        if (c >= 0) ts.template push_node<NW>(x);
+        if (++c >= Pr::wots_len) break;
+        load_node<S>(wsig + c * Pr::n, x);
+        s = wots_digit<S>(root, c);
+        adrs_set_chain_hash(wa, (uint32_t)c, 0);
+        const uint32_t W04[5] = {wa.w0, wa.w1, wa.w2, wa.w3, wa.w4};
+#pragma unroll
+        for (int j = 0; j < 8; j++) pre5[j] = mid[j];
+        rounds_prefix<V, 5>(pre5, W04);  // chain-invariant rounds 0-4 (as chain_F)
+      }
+      if (c >= Pr::wots_len) break;
+      uint32_t W[16];
+      W[0] = wa.w0; W[1] = wa.w1; W[2] = wa.w2; W[3] = wa.w3; W[4] = wa.w4;
+      W[5] = join16(s, x[0]);
+#pragma unroll
+      for (int j = 1; j < NW; j++) W[5 + j] = join16(x[j - 1], x[j]);
+      W[5 + NW] = (x[NW - 1] << 16) | 0x8000u;
+#pragma unroll
+      for (int j = 6 + NW; j < 15; j++) W[j] = 0;
+      W[15] = (uint32_t)((64 + 22 + 4 * NW) * 8);
+      uint32_t st[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) st[j] = mid[j];
+      compress_resume<V, 5>(st, pre5, W);
+#pragma unroll
+      for (int j = 0; j < NW; j++) x[j] = st[j];
+      s++;
+    }
+    ts.finish(22u + (uint32_t)(Pr::wots_len * Pr::n));
+    uint32_t node[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) node[j] = ts.st[j];
+    walk_auth<S, V>(node, mid, make_adrs((uint32_t)layer, tree, ADDR_HASHTREE, 0, 0, 0), leaf_idx, 0,
+                    wsig + Pr::wots_sig_bytes, Pr::hp);
+#pragma unroll
+    for (int j = 0; j < 8; j++) root[j] = node[j];
+    leaf_idx = (uint32_t)(tree & (uint64_t)(Pr::leaves - 1));
+    tree = shr64(tree, Pr::hp);
+  }
+  bool eq = true;
+#pragma unroll
+  for (int j = 0; j < NW; j++) eq = eq && (root[j] == pk_root[j]);
+  a.ok[i] = eq ? 1 : 0;
+}
+
 }  // namespace hs
