@@ -1,20 +1,26 @@
 // hs_kernels.cuh -- the B200 signing kernels (templated on parameter set S
 // and SHA-256 arithmetic path V).
 //
-//   key_setup   per key: PK.seed midstate, HMAC ipad/opad midstates
-//               (hashes.py:79-88 precomputation, done once per key on device)
-//   msg_prep    per message: R = PRF_msg, H_msg, MGF1, tree/leaf/FORS indices
-//               (hashes.py:152-191, sigcore.py:75-121)
-//   fors_sign   FORS_Sign with the paper's Tree Fusion: a CTA owns F fused
-//               sets of N_tree trees (vexec.py:319-473, FusedSetLayout
-//               vexec.py:130-181, Relax vexec.py:115-127)
-//   fors_pk     T_k over the k FORS roots (vexec.py:476-481)
-//   tree_sign   TREE_Sign: one thread per hypertree leaf runs the full WOTS
-//               leaf (wots.py:119-143); the subtree is reduced with warp
-//               shuffles (vexec.py:492-551 / oracle.py:27-63)
-//   wots_sign   WOTS+_Sign: one thread per (layer, chain) (parallel.py:31-59)
-//   keygen_root root of layer d-1, tree 0 (oracle.py:216-226)
-//   verify      one warp per message (sigcore.py:181-221)
+//   key_setup    per key: PK.seed midstate, HMAC ipad/opad midstates, PRF
+//                state after SK.seed (hashes.py:79-88 precomputation, on device)
+//   msg_prep     per message: R = PRF_msg, H_msg, MGF1, tree/leaf/FORS indices
+//                (hashes.py:152-191, sigcore.py:75-121), shared-subtree flags
+//   fors_sign    FORS_Sign with the paper's Tree Fusion: a CTA owns F fused
+//                sets of N_tree trees (vexec.py:319-473, FusedSetLayout
+//                vexec.py:130-181, Relax vexec.py:115-127), levels up to
+//                fors_cta_levels in shared memory
+//   fors_level   one upper FORS level for the whole batch
+//   fors_pk      T_k over the k FORS roots (vexec.py:476-481)
+//   tree_chain   TREE_Sign part 1: one thread per WOTS chain (wots.py:42-65)
+//   tree_root    TREE_Sign part 2: one thread per hypertree leaf: T_len over
+//                the chain ends, warp-shuffle Merkle reduction
+//                (wots.py:119-143, vexec.py:492-551 / oracle.py:27-63)
+//   tree_sign    fused TREE_Sign (thread = leaf runs its chains), tree_split=0
+//   shared_*     the top layers' subtrees, once per batch (both shapes)
+//   wots_gather  WOTS+_Sign from the chain nodes TREE_Sign recorded;
+//   wots_sign    WOTS+_Sign recomputing its chains (parallel.py:31-59)
+//   keygen_root  root of layer d-1, tree 0 (oracle.py:216-226)
+//   verify       one thread per signature (sigcore.py:181-221)
 //
 // Every output byte equals the reference's sigcore.sign for the same inputs.
 #pragma once
@@ -1200,7 +1206,6 @@ __global__ void __launch_bounds__(kTreeBlock) keygen_root_kernel(LaunchArgs a) {
 // compute_root oracle.py:66-95).  FORS trees and WOTS chains spread over the
 // lanes; the serial T_k / T_len / auth-path walks run on lane 0.
 // ---------------------------------------------------------------------------
-constexpr int kVerifyWarps = 4;
 
 template <int S>
 __device__ __forceinline__ void load_node(const uint8_t* p, uint32_t* x) {
@@ -1230,139 +1235,11 @@ __device__ __forceinline__ void walk_auth(uint32_t node[8], const uint32_t mid[8
   }
 }
 
-template <int S, class V>
-__global__ void __launch_bounds__(32 * kVerifyWarps) verify_kernel(LaunchArgs a) {
-  using Pr = P<S>;
-  constexpr int NW = Pr::NW;
-  __shared__ uint32_t s_ends[kVerifyWarps][Pr::wots_len > Pr::k ? Pr::wots_len * NW : Pr::k * NW];
-  __shared__ uint32_t s_col[kVerifyWarps][32];
-  __shared__ uint32_t s_root[kVerifyWarps][8];
-  __shared__ uint32_t s_mid[kVerifyWarps][8];
-  __shared__ uint64_t s_tree[kVerifyWarps];
-  __shared__ uint32_t s_leaf[kVerifyWarps];
-  __shared__ uint16_t s_idx[kVerifyWarps][Pr::k];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t i = blockIdx.x * kVerifyWarps + warp;
-  if (i >= a.count) return;  // whole warp exits together
-  const uint32_t key = a.key_idx ? a.key_idx[i] : 0u;
-  const uint8_t* pk = a.pks + (size_t)key * 2 * Pr::n;
-  const uint8_t* sig = a.vsigs + (size_t)i * Pr::sig_bytes;
-  uint32_t pk_seed[8], pk_root[8];
-  for (int j = 0; j < 8; j++) {
-    pk_seed[j] = j < NW ? load_be(pk + 4 * j) : 0u;
-    pk_root[j] = j < NW ? load_be(pk + Pr::n + 4 * j) : 0u;
-  }
-  if (lane == 0) {
-    uint32_t mid[8], W[16];
-    for (int j = 0; j < 8; j++) mid[j] = IVc(j);
-    for (int j = 0; j < 16; j++) W[j] = j < NW ? pk_seed[j] : 0u;
-    compress<V>(mid, W);
-    for (int j = 0; j < 8; j++) s_mid[warp][j] = mid[j];
-    // H_msg with R = sig[0:n] (hashes.py:175-191)
-    uint32_t R[8], dig0[8];
-    for (int j = 0; j < 8; j++) R[j] = j < NW ? load_be(sig + 4 * j) : 0u;
-    const uint8_t* msg = a.msgs + a.offs[i];
-    const uint64_t mlen = a.offs[i + 1] - a.offs[i];
-    {  // word-level, as msg_prep (sha_prefix_msg)
-      uint32_t pre[3 * NW];
-      for (int j = 0; j < NW; j++) { pre[j] = R[j]; pre[NW + j] = pk_seed[j]; pre[2 * NW + j] = pk_root[j]; }
-      for (int j = 0; j < 8; j++) dig0[j] = IVc(j);
-      sha_prefix_msg<V, 3 * NW>(dig0, 0, pre, msg, mlen);
-    }
-    uint8_t dg[64];
-    constexpr int nctr = (Pr::digest_bytes + 31) / 32;
-    for (int c = 0; c < nctr; c++) {
-      uint32_t pre[2 * NW + 9], o[8];
-      for (int j = 0; j < NW; j++) { pre[j] = R[j]; pre[NW + j] = pk_seed[j]; }
-      for (int j = 0; j < 8; j++) { pre[2 * NW + j] = dig0[j]; o[j] = IVc(j); }
-      pre[2 * NW + 8] = (uint32_t)c;
-      sha_prefix_msg<V, 2 * NW + 9>(o, 0, pre, msg, 0);
-      for (int j = 0; j < 32; j++) dg[32 * c + j] = (uint8_t)(o[j >> 2] >> (24 - 8 * (j & 3)));
-    }
-    uint64_t tree = 0;
-    for (int j = 0; j < Pr::tree_bytes; j++) tree = (tree << 8) | dg[Pr::fors_msg_bytes + j];
-    if (Pr::tree_bits < 64) tree &= (1ull << (Pr::tree_bits < 64 ? Pr::tree_bits : 63)) - 1ull;
-    uint32_t leaf = 0;
-    for (int j = 0; j < Pr::leaf_bytes; j++) leaf = (leaf << 8) | dg[Pr::fors_msg_bytes + Pr::tree_bytes + j];
-    leaf &= (1u << Pr::leaf_bits) - 1u;
-    s_tree[warp] = tree;
-    s_leaf[warp] = leaf;
-    int off = 0;
-    for (int g = 0; g < Pr::k; g++) {
-      uint32_t v = 0;
-      for (int j = 0; j < Pr::log_t; j++, off++) v |= (uint32_t)((dg[off >> 3] >> (off & 7)) & 1) << j;
-      s_idx[warp][g] = (uint16_t)v;
-    }
-  }
-  __syncwarp();
-  uint32_t mid[8];
-  for (int j = 0; j < 8; j++) mid[j] = s_mid[warp][j];
-  uint64_t tree = s_tree[warp];
-  uint32_t leaf_idx = s_leaf[warp];
-
-  // FORS public key from the signature
-  const uint8_t* fsig = sig + Pr::off_fors;
-  constexpr int tree_sig = (1 + Pr::log_t) * Pr::n;
-  for (int g = lane; g < Pr::k; g += 32) {
-    const uint32_t sel = s_idx[warp][g];
-    Adrs fa = make_adrs(0, tree, ADDR_FORS_TREE, leaf_idx, 0, (uint32_t)(g * Pr::t) + sel);
-    uint32_t sk[NW], node[8];
-    load_node<S>(fsig + g * tree_sig, sk);
-    thash_reg<V, NW>(node, mid, fa, sk);
-    walk_auth<S, V>(node, mid, fa, sel, (uint32_t)(g * Pr::t), fsig + g * tree_sig + Pr::n, Pr::log_t);
-    for (int j = 0; j < NW; j++) s_ends[warp][g * NW + j] = node[j];
-  }
-  __syncwarp();
-  if (lane == 0) {
-    TStream<V> ts;
-    ts.begin(mid, make_adrs(0, tree, ADDR_FORS_ROOTS, leaf_idx, 0, 0), s_col[warp], 1);
-    for (int g = 0; g < Pr::k; g++) ts.template push_node<NW>(&s_ends[warp][g * NW]);
-    ts.finish(22u + (uint32_t)(Pr::k * Pr::n));
-    for (int j = 0; j < NW; j++) s_root[warp][j] = ts.st[j];
-  }
-  __syncwarp();
-
-  const uint8_t* ht = sig + Pr::off_ht;
-#pragma unroll 1
-  for (int layer = 0; layer < Pr::d; layer++) {
-    uint32_t root[8];
-    for (int j = 0; j < NW; j++) root[j] = s_root[warp][j];
-    const uint8_t* wsig = ht + (size_t)layer * Pr::layer_bytes;
-    for (int c = lane; c < Pr::wots_len; c += 32) {
-      const uint32_t digit = wots_digit<S>(root, c);
-      uint32_t x[8];
-      load_node<S>(wsig + c * Pr::n, x);
-      Adrs wa = make_adrs((uint32_t)layer, tree, ADDR_WOTS, leaf_idx, (uint32_t)c, 0);
-      chain_F<V, NW>(x, mid, wa, digit, (uint32_t)(Pr::w - 1) - digit);
-      for (int j = 0; j < NW; j++) s_ends[warp][c * NW + j] = x[j];
-    }
-    __syncwarp();
-    if (lane == 0) {
-      TStream<V> ts;
-      ts.begin(mid, make_adrs((uint32_t)layer, tree, ADDR_WOTS_PK, leaf_idx, 0, 0), s_col[warp], 1);
-      for (int c = 0; c < Pr::wots_len; c++) ts.template push_node<NW>(&s_ends[warp][c * NW]);
-      ts.finish(22u + (uint32_t)(Pr::wots_len * Pr::n));
-      uint32_t node[8];
-      for (int j = 0; j < 8; j++) node[j] = ts.st[j];
-      walk_auth<S, V>(node, mid, make_adrs((uint32_t)layer, tree, ADDR_HASHTREE, 0, 0, 0), leaf_idx, 0,
-                      wsig + Pr::wots_sig_bytes, Pr::hp);
-      for (int j = 0; j < NW; j++) s_root[warp][j] = node[j];
-    }
-    __syncwarp();
-    leaf_idx = (uint32_t)(tree & (uint64_t)(Pr::leaves - 1));
-    tree = shr64(tree, Pr::hp);
-  }
-  if (lane == 0) {
-    bool eq = true;
-    for (int j = 0; j < NW; j++) eq = eq && (s_root[warp][j] == pk_root[j]);
-    a.ok[i] = eq ? 1 : 0;
-  }
-}
-
 // ---------------------------------------------------------------------------
-// verify_thread_kernel: one thread per signature (sigcore.py:181-221).  The
-// warp-per-message kernel above leaves 31 lanes idle through every T_len and
-// auth walk and runs 35-67 chains of unequal length on 32 lanes; here each
+// verify_thread_kernel: one thread per signature (sigcore.py:181-221).  A
+// warp-per-message kernel (round-1 first version) left 31 lanes idle through
+// every T_len and auth walk and ran 35-67 chains of unequal length on 32
+// lanes (1.8-2.4x slower, profiles/r01f_stress_verify_thread.txt); here each
 // thread walks its own signature and the wots_len chains of a layer as ONE
 // flattened loop of F steps (sum of 15 - digit over the chains, nearly the
 // same count for every thread), pushing each chain end into its T_len stream

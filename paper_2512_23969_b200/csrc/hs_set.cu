@@ -50,11 +50,7 @@ cudaError_t launch_kernel<HS_SET>(int which, int variant, const LaunchArgs& a, c
                               s>>>(a);
       return cudaGetLastError();
     case K_VERIFY:
-#ifdef HS_VERIFY_WARP
-      verify_kernel<S, Native><<<blocks_for(a.count, kVerifyWarps), 32 * kVerifyWarps, 0, s>>>(a);
-#else
       verify_thread_kernel<S, Native><<<blocks_for(a.count, kVerifyThreads), kVerifyThreads, 0, s>>>(a);
-#endif
       return cudaGetLastError();
     default:
       break;
