@@ -323,7 +323,10 @@ int ensure_capacity(hs_t* h, int set, uint32_t count, size_t msg_bytes) {
 // level 1, so 0 means 1), or auto (-1): the measured best on B200 for every
 // tuned layout was to hand everything above the leaf phase to the grids
 // (tools/fors_split.py, profiles/r01_fors_split.txt).
-int fors_cta_levels(int set, const hs_set_config& c) {
+// (Keeping the whole tree in the CTA for small batches was measured slower,
+// not faster: 1 message 124 -> 133 us, 64 messages 442 -> 519 us for 128f.)
+int fors_cta_levels(int set, const hs_set_config& c, uint32_t count) {
+  (void)count;
   const SetInfo& I = kInfo[set];
   const int lowest = c.fors_relax ? 1 : 0;
   if (c.fors_cta_levels < 0) return lowest;
@@ -333,7 +336,7 @@ int fors_cta_levels(int set, const hs_set_config& c) {
 // words of fors_nodes[b]: buffer 0 holds levels Lc, Lc+2, ..., buffer 1 Lc+1, ...
 size_t fors_node_words(int set, const hs_set_config& c, uint32_t count, int b) {
   const SetInfo& I = kInfo[set];
-  const int L = fors_cta_levels(set, c);
+  const int L = fors_cta_levels(set, c, count);
   return L >= I.log_t ? 0 : (size_t)count * I.k * ((size_t)I.t >> (L + b)) * (I.n / 4);
 }
 
@@ -367,7 +370,7 @@ LaunchArgs make_args(hs_t* h, int set, uint32_t first, uint32_t count) {
   a.fors_trees_per_set = St.cfg.fors_trees_per_set;
   a.fors_sets_fused = St.cfg.fors_sets_fused;
   a.fors_relax = St.cfg.fors_relax;
-  a.fors_cta_levels = fors_cta_levels(set, St.cfg);
+  a.fors_cta_levels = fors_cta_levels(set, St.cfg, count);
   if (a.fors_cta_levels < I.log_t) {
     for (int b = 0; b < 2; b++)
       a.fors_nodes[b] = B.fnodes[b] + (size_t)first * I.k * ((size_t)I.t >> (a.fors_cta_levels + b)) * (I.n / 4);
@@ -1089,7 +1092,7 @@ int hs_batch_info(hs_t* h, int set, int32_t* out, int cap) {
     CUDA_TRY(h, cudaMemcpy(f.data(), B.key_used + St.nkeys, f.size(), cudaMemcpyDeviceToHost));
     for (uint8_t x : f) built += x != 0;
   }
-  const int32_t v[5] = {(int32_t)St.staged, St.shared_eff, fors_cta_levels(set, St.cfg), St.cfg.tree_split, built};
+  const int32_t v[5] = {(int32_t)St.staged, St.shared_eff, fors_cta_levels(set, St.cfg, St.staged), St.cfg.tree_split, built};
   const int n = std::min(cap, 5);
   for (int i = 0; i < n; i++) out[i] = v[i];
   return n;

@@ -115,8 +115,8 @@ def test_fors_upper_levels_split(eng, oracle_mod, set_id):
     p = derive(set_id)
     rng = random.Random(1234)
     sk = oracle_mod.keygen(set_id, rng.randbytes(3 * p.n))
-    msgs = [rng.randbytes(rng.choice([0, 32, 77])) for _ in range(5)]
-    ref = [oracle_mod.sign(set_id, sk, m) for m in msgs]
+    msgs = [rng.randbytes(rng.choice([0, 32, 77])) for _ in range(300)]
+    ref, _ = oracle_mod.sign_many(set_id, sk, None, msgs)
     eng.upload_keys(set_id, sk)
     base = eng.config(set_id)
     try:
@@ -137,8 +137,8 @@ def test_config_change_rebuilds_graph(eng, oracle_mod):
     p = derive(set_id)
     rng = random.Random(77)
     sk = oracle_mod.keygen(set_id, rng.randbytes(3 * p.n))
-    msgs = [rng.randbytes(32) for _ in range(3)]
-    ref = [oracle_mod.sign(set_id, sk, m) for m in msgs]
+    msgs = [rng.randbytes(32) for _ in range(300)]
+    ref, _ = oracle_mod.sign_many(set_id, sk, None, msgs)
     eng.upload_keys(set_id, sk)
     base = eng.config(set_id)
     try:
