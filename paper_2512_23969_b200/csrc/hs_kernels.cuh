@@ -197,7 +197,7 @@ __global__ void msg_prep_kernel(LaunchArgs a) {
 #pragma unroll
     for (int j = 9; j < 15; j++) W[j] = 0;
     W[15] = (64 + 32) * 8;
-    compress<V>(R, W);
+    compress_compact<V>(R, W);
   }
   uint8_t* sig = a.sigs + (size_t)i * Pr::sig_bytes;
   store_node<NW>(sig, R);

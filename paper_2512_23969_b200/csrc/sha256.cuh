@@ -257,6 +257,42 @@ __device__ __forceinline__ void compress(uint32_t st[8], uint32_t W[16]) {
   for (int i = 0; i < 8; i++) st[i] = v.ff(st[i], s[i]);
 }
 
+// Compact compression for latency-bound single-thread code (message
+// preparation, verification prologue): the 64 rounds as a 4-trip loop over a
+// 16-round unrolled body with K from constant memory, so the code is ~4x
+// smaller than the fully unrolled compress (whose instruction fetch, not its
+// arithmetic, dominates a lone warp's hash chain).  Same result as compress.
+static __constant__ uint32_t c_K[64] = {
+    0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
+    0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
+    0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
+    0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
+    0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
+    0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
+    0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
+    0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2,
+};
+template <class V>
+__device__ __noinline__ void compress_compact(uint32_t st[8], const uint32_t Win[16]) {
+  uint32_t W[16];
+#pragma unroll
+  for (int j = 0; j < 16; j++) W[j] = Win[j];
+  const V v{};
+  uint32_t a = st[0], b = st[1], c = st[2], d = st[3], e = st[4], f = st[5], g = st[6], h = st[7];
+#pragma unroll 1
+  for (int r = 0; r < 64; r += 16) {
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      if (r > 0) W[j] = v.wnew(v.s1(W[(j + 14) & 15]), W[(j + 9) & 15], v.s0(W[(j + 1) & 15]), W[j]);
+      const uint32_t t = v.t1(h, c_K[r + j], W[j], v.S1(e), ch(e, f, g));
+      const uint32_t an = v.anew(t, v.S0(a), maj(a, b, c));
+      h = g; g = f; f = e; e = v.enew(d, t);
+      d = c; c = b; b = a; a = an;
+    }
+  }
+  st[0] += a; st[1] += b; st[2] += c; st[3] += d; st[4] += e; st[5] += f; st[6] += g; st[7] += h;
+}
+
 // Rounds [0, R) only (no schedule expansion needed while R <= 16).
 template <class V, int R>
 __device__ __forceinline__ void rounds_prefix(uint32_t s[8], const uint32_t* W) {
@@ -581,7 +617,7 @@ __device__ __forceinline__ void sha_prefix_msg(uint32_t st[8], uint64_t absorbed
       W[j] = k < P ? pre[k < P ? k : 0] : msg_word(m, mlen, (uint64_t)(k - P));
     }
     if ((uint64_t)b == nblk - 1) { W[14] = (uint32_t)(bits >> 32); W[15] = (uint32_t)bits; }
-    compress<V>(st, W);
+    compress_compact<V>(st, W);
   }
 #pragma unroll 1
   for (uint64_t b = PB; b < nblk; b++) {
@@ -589,7 +625,7 @@ __device__ __forceinline__ void sha_prefix_msg(uint32_t st[8], uint64_t absorbed
 #pragma unroll
     for (int j = 0; j < 16; j++) W[j] = msg_word(m, mlen, 16 * b + j - P);
     if (b == nblk - 1) { W[14] = (uint32_t)(bits >> 32); W[15] = (uint32_t)bits; }
-    compress<V>(st, W);
+    compress_compact<V>(st, W);
   }
 }
 
@@ -620,7 +656,7 @@ __device__ __forceinline__ void sha_prefix_words(uint32_t st[8], uint64_t absorb
       W[j] = k < P ? pre[k < P ? k : 0] : (k - P < 17 ? mw[k - P < 17 ? k - P : 0] : 0u);
     }
     if ((uint32_t)b == nblk - 1) { W[14] = (uint32_t)(bits >> 32); W[15] = (uint32_t)bits; }
-    compress<V>(st, W);
+    compress_compact<V>(st, W);
   }
 }
 
