@@ -501,8 +501,11 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
 }
 
 // Messages [first, first + cn) of sub-batch j of T.  The last sub-batch gets
-// half the share of the others (weights 2, ..., 2, 1): only its D2H copy is
-// not hidden under later compute in hs_sign_batch, so it is kept small.
+// a smaller share than the others (weights H, ..., H, 1): only its D2H copy
+// is not hidden under later compute in hs_sign_batch, so it is kept small.
+#ifndef HS_SUB_HEAD_WEIGHT
+#define HS_SUB_HEAD_WEIGHT 4
+#endif
 void sub_range(uint32_t count, int T, int j, uint32_t& first, uint32_t& cn) {
 #ifdef HS_EQUAL_SUBBATCH
   const uint32_t per = (count + T - 1) / T;
@@ -514,8 +517,9 @@ void sub_range(uint32_t count, int T, int j, uint32_t& first, uint32_t& cn) {
     cn = count;
     return;
   }
-  const uint64_t W = 2ull * (uint64_t)T - 1ull;
-  auto edge = [&](int i) { return (uint32_t)((uint64_t)count * std::min<uint64_t>(2ull * (uint64_t)i, W) / W); };
+  const uint64_t H = HS_SUB_HEAD_WEIGHT;  // weight of every sub-batch but the last (which has weight 1)
+  const uint64_t W = H * ((uint64_t)T - 1ull) + 1ull;
+  auto edge = [&](int i) { return (uint32_t)((uint64_t)count * std::min<uint64_t>(H * (uint64_t)i, W) / W); };
   first = edge(j);
   cn = edge(j + 1) - first;
 #endif
