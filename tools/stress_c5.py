@@ -31,7 +31,7 @@ import paper_2512_23969_b200 as hs  # noqa: E402
 from paper_2512_23969_b200.engine import PinnedBuffer, pack_messages  # noqa: E402
 
 
-def run_set(eng, set_id: str, messages: int, nkeys: int, chunk: int) -> dict:
+def run_set(eng, set_id: str, messages: int, nkeys: int, chunk: int, extra: int = 0) -> dict:
     p = hs.derive(set_id)
     rng = random.Random(2512_23969 + 5)
     seeds = [rng.randbytes(3 * p.n) for _ in range(nkeys)]
@@ -65,6 +65,9 @@ def run_set(eng, set_id: str, messages: int, nkeys: int, chunk: int) -> dict:
         verified += cn
         # oracle check: first message of every key not yet checked in this chunk
         todo = [i for i in range(cn) if int(kidx[i]) not in per_key_checked][: nkeys]
+        if extra:  # plus a random sample of the chunk
+            pick = random.Random(c0).sample(range(cn), min(extra, cn))
+            todo = sorted(set(todo) | set(pick))
         if todo:
             ref, _ = oracle.sign_many(set_id, b"".join(sks), [int(kidx[i]) for i in todo], [msgs[i] for i in todo])
             for i, r in zip(todo, ref):
@@ -85,11 +88,12 @@ def main():
     ap.add_argument("--keys", type=int, default=1024)
     ap.add_argument("--chunk", type=int, default=65536)
     ap.add_argument("--sets", default="128f,192f,256f")
+    ap.add_argument("--oracle-extra", type=int, default=0, help="extra random messages per chunk checked vs the oracle")
     a = ap.parse_args()
     oracle.build()
     eng = hs.get_engine(int(os.environ.get("LOCAL_RANK", "0")))
     for set_id in a.sets.split(","):
-        print(json.dumps(run_set(eng, set_id, a.messages, a.keys, a.chunk)), flush=True)
+        print(json.dumps(run_set(eng, set_id, a.messages, a.keys, a.chunk, a.oracle_extra)), flush=True)
 
 
 if __name__ == "__main__":
