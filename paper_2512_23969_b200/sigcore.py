@@ -95,10 +95,14 @@ def _apply_overrides(eng, p, fusion, relax, selection) -> dict | None:
     if relax is not None:
         kw["fors_relax"] = bool(getattr(relax, "enabled", relax))
     if selection is not None:
+        # reference backends (backends.py:201-257): "baseline" -> the native path;
+        # "tuned" -> the path the on-device tuner chose for this kernel (the
+        # configured one), or the fast path where the config says native
         var = {}
         for kernel in ("FORS_Sign", "TREE_Sign", "WOTS_Sign"):
             b = selection.get(kernel, p.id)
-            var[kernel] = 1 if str(getattr(b, "value", b)) == "tuned" else 0
+            tuned = str(getattr(b, "value", b)) == "tuned"
+            var[kernel] = (before["variant"][kernel] or 1) if tuned else 0
         kw["variant"] = var
     eng.set_config(p.id, **kw)
     return before

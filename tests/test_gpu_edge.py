@@ -113,3 +113,28 @@ def test_verify_into_pinned_roundtrip(eng, oracle_mod):
         assert raw[:p.sig_bytes] == oracle_mod.sign(set_id, sk, msgs[0])
     finally:
         out.free()
+
+
+def test_reference_call_knobs(eng, oracle_mod):
+    """sigcore.sign's per-call fusion / relax / selection knobs (sigcore.py:139-153)
+    change only the execution shape: same bytes, engine config restored."""
+
+    class Selection:  # duck-typed reference BackendSelection (backends.py:201-257)
+        def __init__(self, v):
+            self.v = v
+
+        def get(self, kernel, set_id):
+            return self.v
+
+    set_id = "192f"
+    p = derive(set_id)
+    seed = random.Random(55).randbytes(3 * p.n)
+    sk = hs.keygen(set_id, seed)
+    msg = b"per-call knobs"
+    ref = oracle_mod.sign(set_id, sk.to_bytes(), msg)
+    base = eng.config(set_id)
+    for sel in (Selection("baseline"), Selection("tuned")):
+        assert hs.sign(msg, sk, set_id, selection=sel) == ref
+    fusion = type("Fusion", (), {"trees_per_set": 2, "sets_fused": 3})()
+    assert hs.sign(msg, sk, set_id, fusion=fusion, relax=True) == ref
+    assert hs.get_engine().config(set_id) == base
