@@ -1255,8 +1255,8 @@ __global__ void __launch_bounds__(kVerifyThreads) verify_thread_kernel(LaunchArg
   const uint32_t i = blockIdx.x * kVerifyThreads + threadIdx.x;
   if (i >= a.count) return;
   uint32_t* mycol = col + threadIdx.x;
-  const uint32_t key = a.key_idx ? a.key_idx[i] : 0u;
-  const uint8_t* pk = a.pks + (size_t)key * 2 * Pr::n;
+  const uint8_t* pk = a.pks;
+  if (a.key_idx) pk += (size_t)a.key_idx[i] * 2 * Pr::n;
   const uint8_t* sig = a.vsigs + (size_t)i * Pr::sig_bytes;
   uint32_t pk_seed[8], pk_root[8], mid[8];
 #pragma unroll
