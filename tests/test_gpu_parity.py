@@ -280,6 +280,11 @@ def test_subtree_sharing(eng, oracle_mod, set_id):
         for L in range(top + 1):
             eng.set_config(set_id, shared_layers=L, shared_auto=False)
             assert eng.sign_batch(set_id, msgs, key_idx=kidx) == ref, L
+            info = eng.batch_info(set_id)
+            if info["shared_layers"]:
+                # only the subtrees some message reads are built: <= one per (key, layer) per message
+                assert 0 < info["shared_subtrees_built"] <= min(2 * hs.params.shared_units(p, info["shared_layers"]),
+                                                                 count * info["shared_layers"])
         eng.set_config(set_id, shared_layers=top, shared_auto=True)
         assert eng.sign_batch(set_id, msgs, key_idx=kidx) == ref
         with pytest.raises(hs.ConfigError):
