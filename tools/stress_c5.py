@@ -89,10 +89,13 @@ def main():
     ap.add_argument("--chunk", type=int, default=65536)
     ap.add_argument("--sets", default="128f,192f,256f")
     ap.add_argument("--oracle-extra", type=int, default=0, help="extra random messages per chunk checked vs the oracle")
+    ap.add_argument("--engine-chunk", type=int, default=0, help="override the engine's messages per device pass")
     a = ap.parse_args()
     oracle.build()
     eng = hs.get_engine(int(os.environ.get("LOCAL_RANK", "0")))
     for set_id in a.sets.split(","):
+        if a.engine_chunk:
+            eng.set_config(set_id, chunk=a.engine_chunk)
         print(json.dumps(run_set(eng, set_id, a.messages, a.keys, a.chunk, a.oracle_extra)), flush=True)
 
 
