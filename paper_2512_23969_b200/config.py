@@ -2,22 +2,24 @@
 
 The file keeps the reference's schema -- per set {fusion, padding, backends,
 relax} plus seme_per_block / worker_width -- so a reference config loads
-unchanged, and adds an optional "b200" block per set carrying what the
-on-device tuner measured: the kernel layout actually used (trees per set,
-fused sets, relax), the SHA-256 path per kernel, WOTS-from-TREE and the
-batch chunk.  ``HERO_SIGN_CONFIG`` overrides the path as in the reference.
+unchanged (its fusion / relax row then sets the FORS layout), and adds an
+optional "b200" block per set carrying what the on-device tuner measured:
+the kernel layout actually used (trees per set, fused sets, relax), the
+SHA-256 path per kernel, WOTS-from-TREE and the batch chunk.  ``HERO_SIGN_CONFIG`` overrides the path as in the reference.
 """
 
 from __future__ import annotations
 
 import json
 import os
+import warnings
 from dataclasses import dataclass, field
 from pathlib import Path
 
 from .errors import ConfigError, FormatError
 from .params import PARAMETER_SETS, derive
-from .tuner import DEFAULT_SEME, FusionCandidate, PaddingScheme, TuneInput, padding_solve, tree_tune
+from .tuner import (B200_FORS_MAX_LANES, DEFAULT_SEME, FusionCandidate, PaddingScheme, TuneInput, padding_solve,
+                    tree_tune)
 
 ENV_CONFIG_PATH = "HERO_SIGN_CONFIG"
 DEFAULT_WORKERS = 4
@@ -95,6 +97,20 @@ class TuningConfig:
         """Push every set's B200 row into an Engine (hs_config_set)."""
         for set_id, cfg in self.sets.items():
             b = dict(cfg.b200) if cfg.b200 else {}
+            if not b:
+                # a reference config (no b200 block): its layout row drives the
+                # FORS kernel -- N_tree and F from `fusion`, Relax from `relax`
+                # (config.py:33-38) -- when the B200 kernel can run it (lanes
+                # within its 768-lane CTA), else the engine keeps its layout
+                p = derive(set_id)
+                lanes = cfg.fusion.trees_per_set * (p.fors_t // 2 if cfg.relax else p.fors_t)
+                if lanes <= B200_FORS_MAX_LANES:
+                    b = {"fors_trees_per_set": cfg.fusion.trees_per_set, "fors_sets_fused": cfg.fusion.sets_fused,
+                         "fors_relax": bool(cfg.relax)}
+                else:
+                    warnings.warn(f"{set_id}: reference layout {cfg.fusion.trees_per_set}x{cfg.fusion.sets_fused} "
+                                  f"needs {lanes} lanes (> {B200_FORS_MAX_LANES}); keeping the engine's layout",
+                                  stacklevel=2)
             kw = {}
             for key in ("fors_trees_per_set", "fors_sets_fused", "fors_relax", "wots_from_tree", "chunk", "streams",
                         "shared_layers", "shared_auto", "fors_cta_levels", "tree_split"):

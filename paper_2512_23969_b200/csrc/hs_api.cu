@@ -877,6 +877,9 @@ int hs_keys_upload(hs_t* h, int set, const uint8_t* sks, uint32_t nkeys) {
   CUDA_TRY(h, launch(set, K_KEYSETUP, St.cfg.variant[3], a, h->s0));
   h->launches++;
   CUDA_TRY(h, cudaStreamSynchronize(h->s0));
+  // a staged batch's key_idx was checked against the previous table: a smaller
+  // table invalidates it (hs_run would index past the new one)
+  if (nkeys < St.nkeys && St.has_keyidx) St.staged = 0;
   St.nkeys = nkeys;
   return HS_OK;
 }
@@ -920,7 +923,9 @@ int hs_stage(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, const 
   if (!h || !valid_set(set) || !offs || (!msgs && count && offs[count] != offs[0]))
     return fail(h, HS_E_USAGE, "bad arguments");
   if (h->sets[set].nkeys == 0) return fail(h, HS_E_NOKEYS, "no keys uploaded for this parameter set");
-  if (offs[count] < offs[0]) return fail(h, HS_E_USAGE, "offsets must be non-decreasing");
+  // every offset, as hs_sign_batch does: msg_prep reads offs[i+1] - offs[i] bytes
+  for (uint32_t i = 0; i < count; i++)
+    if (offs[i + 1] < offs[i]) return fail(h, HS_E_USAGE, "offsets must be non-decreasing");
   CUDA_TRY(h, cudaSetDevice(h->device));
   return stage_inputs(h, set, msgs, offs, key_idx, opt_rand, 0, count);
 }

@@ -105,6 +105,15 @@ __device__ __forceinline__ void store_node(uint8_t* p, const uint32_t* x) {
   for (int j = 0; j < NW; j++) store_be(p + 4 * j, x[j]);
 }
 
+// Store one of two register-resident nodes chosen at run time: a per-word
+// select keeps both in registers (passing `first ? a : b` as a pointer makes
+// ptxas place the arrays in local memory).
+template <int NW>
+__device__ __forceinline__ void store_node_sel(uint8_t* p, bool first, const uint32_t* a, const uint32_t* b) {
+#pragma unroll
+  for (int j = 0; j < NW; j++) store_be(p + 4 * j, first ? a[j] : b[j]);
+}
+
 __device__ __forceinline__ uint32_t load_be(const uint8_t* p) {
   return ((uint32_t)p[0] << 24) | ((uint32_t)p[1] << 16) | ((uint32_t)p[2] << 8) | p[3];
 }
@@ -903,7 +912,7 @@ __global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) 
       fors_leaf<S, V>(mid, sks, fa, pre, (uint32_t)(g * t) + j2 + 1u, sk1, l1);
       if (j2 == sel) store_node<NW>(fsig + g * tree_sig, sk0);
       if (j2 + 1u == sel) store_node<NW>(fsig + g * tree_sig, sk1);
-      if ((sel >> 1) == (uint32_t)lane_leaf) store_node<NW>(fsig + g * tree_sig + Pr::n, (sel & 1u) ? l0 : l1);
+      if ((sel >> 1) == (uint32_t)lane_leaf) store_node_sel<NW>(fsig + g * tree_sig + Pr::n, (sel & 1u) != 0u, l0, l1);
       uint32_t m[2 * NW], par[8];
 #pragma unroll
       for (int j = 0; j < NW; j++) { m[j] = l0[j]; m[NW + j] = l1[j]; }
@@ -953,7 +962,7 @@ __global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) 
       }
       const uint32_t sel = (uint32_t)idx[g] >> (lvl - 1);
       if ((sel >> 1) == (uint32_t)j)
-        store_node<NW>(fsig + g * tree_sig + Pr::n + (lvl - 1) * Pr::n, (sel & 1u) ? m : m + NW);
+        store_node_sel<NW>(fsig + g * tree_sig + Pr::n + (lvl - 1) * Pr::n, (sel & 1u) != 0u, m, m + NW);
       uint32_t par[8];
       Adrs na = fa;
       adrs_set_chain_hash(na, (uint32_t)lvl, (uint32_t)j + ((uint32_t)(g * t) >> lvl));
@@ -1007,7 +1016,7 @@ __global__ void __launch_bounds__(kForsLevelBlock) fors_level_kernel(LaunchArgs 
   const uint32_t sel = (uint32_t)a.indices[(size_t)msg * Pr::k + g] >> (L - 1);
   constexpr int tree_sig = (1 + Pr::log_t) * Pr::n;
   uint8_t* fsig = a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_fors;
-  if ((sel >> 1) == j) store_node<NW>(fsig + g * tree_sig + Pr::n + (L - 1) * Pr::n, (sel & 1u) ? m : m + NW);
+  if ((sel >> 1) == j) store_node_sel<NW>(fsig + g * tree_sig + Pr::n + (L - 1) * Pr::n, (sel & 1u) != 0u, m, m + NW);
   uint32_t mid[8], pre5[8], par[8];
   const uint32_t* lp = a.fors_lpre + ((size_t)msg * (Pr::log_t + 1) + L) * 8;
 #pragma unroll

@@ -41,6 +41,24 @@ def _u8ptr(buf):
     raise UsageError(f"unsupported buffer type {type(buf).__name__}")
 
 
+def _offsets(offs, count: int) -> np.ndarray:
+    """offs as a contiguous uint64 array of at least count + 1 entries (the C
+    side reads exactly count + 1)."""
+    o = np.ascontiguousarray(offs, dtype=np.uint64)
+    if o.ndim != 1 or o.shape[0] < count + 1:
+        raise UsageError(f"offsets must hold count + 1 = {count + 1} entries, got {o.shape}")
+    return o
+
+
+def _key_index(key_idx, count: int) -> np.ndarray | None:
+    if key_idx is None:
+        return None
+    k = np.ascontiguousarray(key_idx, dtype=np.uint32)
+    if k.ndim != 1 or k.shape[0] < count:
+        raise UsageError(f"key_idx must hold one entry per message ({count}), got {k.shape}")
+    return k
+
+
 def pack_messages(msgs: Sequence[bytes]) -> tuple[bytes, np.ndarray]:
     offs = np.zeros(len(msgs) + 1, dtype=np.uint64)
     if msgs:
@@ -59,14 +77,26 @@ class Engine:
         if rc != _lib.HS_OK or not h.value:
             raise HeroSignError(f"hs_open(device={self.device}) failed (rc={rc}): no usable CUDA device")
         self._h = h
-        self._lock = threading.Lock()
+        # One handle is not reentrant (include/herosign_b200.h).  Every call
+        # into the library holds this lock; callers that chain several calls
+        # (upload keys -> override config -> sign -> restore, as sigcore does)
+        # hold ``engine.lock`` across the whole sequence so another thread
+        # cannot swap the key table or the config in between.
+        self._lock = threading.RLock()
         self._keys: dict[str, bytes] = {}
 
     # -- lifecycle -------------------------------------------------------
+    @property
+    def lock(self) -> threading.RLock:
+        """Re-entrant lock serialising this handle's calls (hold it across a
+        multi-call sequence that must see one key table and config)."""
+        return self._lock
+
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and self._h.value:
-            _lib.lib().hs_close(self._h)
-            self._h = None
+            with self._lock:
+                _lib.lib().hs_close(self._h)
+                self._h = None
 
     def __del__(self):  # pragma: no cover - interpreter shutdown ordering
         try:
@@ -85,7 +115,8 @@ class Engine:
 
     def config(self, set_id: str) -> dict:
         c = _lib.SetConfig()
-        self._check(_lib.lib().hs_config_get(self._h, SET_INDEX[set_id], ctypes.byref(c)), "hs_config_get")
+        with self._lock:
+            self._check(_lib.lib().hs_config_get(self._h, SET_INDEX[set_id], ctypes.byref(c)), "hs_config_get")
         return {
             "fors_trees_per_set": c.fors_trees_per_set,
             "fors_sets_fused": c.fors_sets_fused,
@@ -102,6 +133,10 @@ class Engine:
         }
 
     def set_config(self, set_id: str, **kw) -> dict:
+        with self._lock:
+            return self._set_config(set_id, **kw)
+
+    def _set_config(self, set_id: str, **kw) -> dict:
         cur = self.config(set_id)
         variant = dict(cur["variant"])
         variant.update(kw.pop("variant", {}) or {})
@@ -134,9 +169,10 @@ class Engine:
         blob = bytes(blob)
         if not blob or len(blob) % p.sk_bytes:
             raise UsageError(f"key table must be a non-empty multiple of {p.sk_bytes} bytes")
-        if self._keys.get(set_id) == blob:
-            return len(blob) // p.sk_bytes
         with self._lock:
+            if self._keys.get(set_id) == blob:
+                return len(blob) // p.sk_bytes
+            self._keys.pop(set_id, None)
             self._check(_lib.lib().hs_keys_upload(self._h, p.index, _u8ptr(blob), len(blob) // p.sk_bytes),
                         "hs_keys_upload")
             self._keys[set_id] = blob
@@ -161,6 +197,10 @@ class Engine:
                   opt_rand=None) -> None:
         """Zero-copy batch sign: inputs/outputs are caller buffers (pinned ones avoid staging)."""
         p = derive(set_id)
+        offs = _offsets(offs, count)
+        key_idx = _key_index(key_idx, count)
+        if opt_rand is not None and not isinstance(opt_rand, int) and len(opt_rand) < count * p.n:
+            raise UsageError(f"opt_rand must be {p.n} bytes per message")
         with self._lock:
             self._check(
                 _lib.lib().hs_sign_batch(self._h, p.index, _u8ptr(blob), _u8ptr(offs),
@@ -171,11 +211,13 @@ class Engine:
     def sign_batch(self, set_id: str, msgs: Sequence[bytes], key_idx: Sequence[int] | None = None,
                    opt_rand: Sequence[bytes] | bytes | None = None) -> list[bytes]:
         p = derive(set_id)
-        if set_id not in self._keys:
-            raise UsageError("no keys uploaded for this parameter set")
         count = len(msgs)
-        if count == 0:
-            return []
+        with self._lock:
+            if set_id not in self._keys:
+                raise UsageError("no keys uploaded for this parameter set")
+            return self._sign_batch(p, set_id, msgs, count, key_idx, opt_rand) if count else []
+
+    def _sign_batch(self, p, set_id, msgs, count, key_idx, opt_rand) -> list[bytes]:
         blob, offs = pack_messages(msgs)
         kidx = None
         if key_idx is not None:
@@ -233,7 +275,8 @@ class Engine:
         if not pks or len(pks) % p.pk_bytes:
             raise UsageError(f"public keys must be a multiple of {p.pk_bytes} bytes")
         ok = np.zeros(count, dtype=np.uint8)
-        kidx = None if key_idx is None else np.ascontiguousarray(key_idx, dtype=np.uint32)
+        offs = _offsets(offs, count)
+        kidx = _key_index(key_idx, count)
         with self._lock:
             self._check(_lib.lib().hs_verify_batch(self._h, p.index, _u8ptr(bytes(pks)), len(pks) // p.pk_bytes,
                                                    _u8ptr(blob), _u8ptr(offs), _u8ptr(kidx), _u8ptr(sigs),
@@ -244,21 +287,30 @@ class Engine:
     # -- device-resident stages (bench / graph signer) ---------------------
     def stage(self, set_id: str, blob, offs: np.ndarray, count: int, key_idx=None, opt_rand=None) -> None:
         p = derive(set_id)
-        self._check(_lib.lib().hs_stage(self._h, p.index, _u8ptr(blob), _u8ptr(offs), _u8ptr(key_idx),
-                                        _u8ptr(opt_rand), count), "hs_stage")
+        offs = _offsets(offs, count)
+        key_idx = _key_index(key_idx, count)
+        if opt_rand is not None and not isinstance(opt_rand, int) and len(opt_rand) < count * p.n:
+            raise UsageError(f"opt_rand must be {p.n} bytes per message")
+        with self._lock:
+            self._check(_lib.lib().hs_stage(self._h, p.index, _u8ptr(blob), _u8ptr(offs), _u8ptr(key_idx),
+                                            _u8ptr(opt_rand), count), "hs_stage")
 
     def run(self, set_id: str, count: int, mode: int = 0) -> None:
-        self._check(_lib.lib().hs_run(self._h, SET_INDEX[set_id], count, mode), "hs_run")
+        with self._lock:
+            self._check(_lib.lib().hs_run(self._h, SET_INDEX[set_id], count, mode), "hs_run")
 
     def sync(self) -> None:
-        self._check(_lib.lib().hs_sync(self._h), "hs_sync")
+        with self._lock:
+            self._check(_lib.lib().hs_sync(self._h), "hs_sync")
 
     def fetch(self, set_id: str, first: int, count: int, out) -> None:
-        self._check(_lib.lib().hs_fetch(self._h, SET_INDEX[set_id], first, count, _u8ptr(out)), "hs_fetch")
+        with self._lock:
+            self._check(_lib.lib().hs_fetch(self._h, SET_INDEX[set_id], first, count, _u8ptr(out)), "hs_fetch")
 
     def timings(self) -> dict:
         ms = (ctypes.c_float * 5)()
-        n = _lib.lib().hs_timings(self._h, ms, 5)
+        with self._lock:
+            n = _lib.lib().hs_timings(self._h, ms, 5)
         if n < 0:
             self._check(n, "hs_timings")
         names = ("batch", "msg_prep", "FORS_Sign", "TREE_Sign", "WOTS_Sign")
@@ -267,8 +319,10 @@ class Engine:
     def bench_run(self, set_id: str, count: int, steps: int, mode: int = 0, flush_bytes: int = 0) -> list[float]:
         """Per-step device ms of `steps` runs over the staged batch (CUDA events, launching stream)."""
         ms = (ctypes.c_float * steps)()
-        self._check(_lib.lib().hs_bench_run(self._h, SET_INDEX[set_id], count, steps, mode, flush_bytes, ms),
-                    "hs_bench_run")
+        with self._lock:
+            self._check(
+                _lib.lib().hs_bench_run(self._h, SET_INDEX[set_id], count, steps, mode, flush_bytes, ms),
+                "hs_bench_run")
         return [float(x) for x in ms]
 
     @property
@@ -280,7 +334,8 @@ class Engine:
         auto policy, FORS levels kept in the CTA, split TREE_Sign, and the shared
         subtrees its last run computed."""
         v = (ctypes.c_int32 * 5)()
-        n = _lib.lib().hs_batch_info(self._h, SET_INDEX[set_id], v, 5)
+        with self._lock:
+            n = _lib.lib().hs_batch_info(self._h, SET_INDEX[set_id], v, 5)
         if n < 0:
             self._check(n, "hs_batch_info")
         return {"staged": int(v[0]), "shared_layers": int(v[1]), "fors_cta_levels": int(v[2]),
@@ -289,7 +344,8 @@ class Engine:
     def launch_stats(self, reset: bool = True) -> dict:
         """Host-side batch launch latency: cudaGraphLaunch calls since the last reset."""
         v = (ctypes.c_double * 3)()
-        n = _lib.lib().hs_launch_stats(self._h, v, 3, 1 if reset else 0)
+        with self._lock:
+            n = _lib.lib().hs_launch_stats(self._h, v, 3, 1 if reset else 0)
         if n < 0:
             self._check(n, "hs_launch_stats")
         return {"graph_launches": int(v[0]), "mean_us": float(v[1]), "max_us": float(v[2])}

@@ -181,13 +181,17 @@ def sign_batch(
             kk = list(key_idx) if key_idx is not None else [0] * len(msgs)
             opt_rand = [o if o is not None else keys[kk[i]].pk_seed for i, o in enumerate(opt_rand)]
     eng = get_engine()
-    eng.upload_keys(p.id, [k.to_bytes() for k in keys])
-    before = _apply_overrides(eng, p, fusion, relax, selection)
-    try:
-        sigs = eng.sign_batch(p.id, [bytes(m) for m in msgs], key_idx=key_idx, opt_rand=opt_rand)
-    finally:
-        if before is not None:
-            eng.set_config(p.id, **before)
+    # the engine is process-wide: key table, per-call overrides, the sign and
+    # the restore form one critical section, so concurrent callers (threads,
+    # several GraphSigners) never sign under each other's keys or layout
+    with eng.lock:
+        eng.upload_keys(p.id, [k.to_bytes() for k in keys])
+        before = _apply_overrides(eng, p, fusion, relax, selection)
+        try:
+            sigs = eng.sign_batch(p.id, [bytes(m) for m in msgs], key_idx=key_idx, opt_rand=opt_rand)
+        finally:
+            if before is not None:
+                eng.set_config(p.id, **before)
     if ctx_out is not None:
         for m in msgs:
             ctx_out.append(SignContext(p, len(m)))
