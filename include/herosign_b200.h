@@ -14,6 +14,7 @@
  *   hs_keys_upload    HashContext.__init__      hashes.py:57-88 (per-key midstates)
  *   hs_sign_batch     sigcore.sign              sigcore.py:139-178, and the batch
  *                     driver cli bench / execute_graphs  batchgraph.py:110-226
+ *   hs_sign_batch_ex  sigcore.sign + its ctx_out work counter  sigcore.py:166-168
  *   hs_verify_batch   sigcore.verify            sigcore.py:181-221
  *   hs_config_get/set TuningConfig per-set row  config.py:33-60 (fusion, relax,
  *                     backends row backends.py:201-257)
@@ -125,6 +126,17 @@ HS_API int hs_keygen_batch(hs_t *h, int set, const uint8_t *seeds, uint32_t nkey
  * the reference's deterministic default); sigs receives count x sig_bytes. */
 HS_API int hs_sign_batch(hs_t *h, int set, const uint8_t *msgs, const uint64_t *offs, const uint32_t *key_idx,
                   const uint8_t *opt_rand, uint32_t count, uint8_t *sigs);
+
+/* hs_sign_batch plus the exact work count: wots_steps[count] (nullable)
+ * receives, per message, the WOTS_Sign F steps of its signature -- the sum of
+ * the signed base-w digits over all d layers -- which is the only
+ * data-dependent term of the reference's HashContext.compressions
+ * (hashes.py:117-159, sigcore.py:166-168 ctx_out); the host adds the fixed
+ * terms (params.compressions_per_signature).  Chunks of cfg.chunk messages
+ * are pipelined: one chunk's staging and copy-out overlap the next one's
+ * signing. */
+HS_API int hs_sign_batch_ex(hs_t *h, int set, const uint8_t *msgs, const uint64_t *offs, const uint32_t *key_idx,
+                            const uint8_t *opt_rand, uint32_t count, uint8_t *sigs, uint32_t *wots_steps);
 
 /* Batched verification; ok[i] = 1 iff sig i verifies under pk row key_idx[i]
  * (pks: nkeys x 2n = pk_seed||pk_root).  sigs is count x sig_bytes. */

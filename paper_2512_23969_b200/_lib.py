@@ -28,7 +28,7 @@ HS_E_CUDA = -10
 
 EXPORTS = (
     "hs_open", "hs_close", "hs_last_error", "hs_device_info", "hs_params", "hs_config_get", "hs_config_set",
-    "hs_fors_smem_bytes", "hs_keys_upload", "hs_keygen_batch", "hs_sign_batch", "hs_verify_batch",
+    "hs_fors_smem_bytes", "hs_keys_upload", "hs_keygen_batch", "hs_sign_batch", "hs_sign_batch_ex", "hs_verify_batch",
     "hs_stage", "hs_run", "hs_sync", "hs_fetch", "hs_timings", "hs_bench_run", "hs_launch_count", "hs_launch_stats", "hs_variants", "hs_batch_info",
     "hs_host_alloc", "hs_host_free",
 )
@@ -89,6 +89,7 @@ def lib() -> ctypes.CDLL:
         "hs_keys_upload": (ctypes.c_int, [vp, ctypes.c_int, u8p, u32]),
         "hs_keygen_batch": (ctypes.c_int, [vp, ctypes.c_int, u8p, u32, u8p]),
         "hs_sign_batch": (ctypes.c_int, [vp, ctypes.c_int, u8p, vp, vp, u8p, u32, u8p]),
+        "hs_sign_batch_ex": (ctypes.c_int, [vp, ctypes.c_int, u8p, vp, vp, u8p, u32, u8p, vp]),
         "hs_verify_batch": (ctypes.c_int, [vp, ctypes.c_int, u8p, u32, u8p, vp, vp, u8p, u32, u8p]),
         "hs_stage": (ctypes.c_int, [vp, ctypes.c_int, u8p, vp, vp, u8p, u32]),
         "hs_run": (ctypes.c_int, [vp, ctypes.c_int, u32, ctypes.c_int]),

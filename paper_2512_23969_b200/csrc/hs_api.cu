@@ -151,12 +151,26 @@ cudaError_t grow_host(T*& p, size_t& cap, size_t need) {
   return e;
 }
 
-struct Buffers {
+// Per-chunk inputs and outputs, double-buffered: hs_sign_batch stages chunk
+// c+1 (host copy + H2D on the copy stream) and drains chunk c's signatures
+// (D2H on the copy-out streams) while chunk c+1 computes.
+constexpr int kSlots = 2;
+struct Slot {
   uint8_t* msgs = nullptr; size_t msgs_cap = 0;
   uint64_t* offs = nullptr; size_t offs_cap = 0;
   uint32_t* keyidx = nullptr; size_t keyidx_cap = 0;
   uint8_t* optrand = nullptr; size_t optrand_cap = 0;
   uint8_t* sigs = nullptr; size_t sigs_cap = 0;
+  uint32_t* wsteps = nullptr; size_t wsteps_cap = 0;  // WOTS_Sign F steps per message
+  // pinned staging
+  uint8_t* h_msgs = nullptr; size_t h_msgs_cap = 0;
+  uint64_t* h_offs = nullptr; size_t h_offs_cap = 0;
+  uint8_t* h_sigs = nullptr; size_t h_sigs_cap = 0;
+  uint32_t* h_wsteps = nullptr; size_t h_wsteps_cap = 0;
+};
+
+struct Buffers {
+  Slot io[kSlots];
   MsgPlan* plans = nullptr; size_t plans_cap = 0;
   uint16_t* idx = nullptr; size_t idx_cap = 0;
   uint32_t* roots = nullptr; size_t roots_cap = 0;
@@ -175,10 +189,6 @@ struct Buffers {
   uint8_t* v_ok = nullptr; size_t v_ok_cap = 0;
   uint64_t* v_offs = nullptr; size_t v_offs_cap = 0;
   uint32_t* v_kidx = nullptr; size_t v_kidx_cap = 0;
-  // pinned staging
-  uint8_t* h_msgs = nullptr; size_t h_msgs_cap = 0;
-  uint64_t* h_offs = nullptr; size_t h_offs_cap = 0;
-  uint8_t* h_sigs = nullptr; size_t h_sigs_cap = 0;
   uint64_t gen = 0;  // bumps whenever a device pointer changes (graph invalidation)
 };
 
@@ -189,7 +199,8 @@ struct SetState {
   uint32_t nkeys = 0;
   uint8_t* sk_raw = nullptr;
   size_t sk_raw_cap = 0;
-  // staged batch
+  // staged batch (in io slot `slot`)
+  int slot = 0;
   uint32_t staged = 0;
   bool has_keyidx = false, has_optrand = false;
   int shared_eff = 0;  // subtree-sharing depth chosen for the staged batch
@@ -220,9 +231,12 @@ struct hs_ctx {
   int sm_count = 0, smem_optin = 0, cc_major = 0, cc_minor = 0;
   void* flush = nullptr;
   size_t flush_cap = 0;
-  cudaStream_t ls[kMaxStreams] = {};   // D2H copy streams
+  cudaStream_t ls[kMaxStreams] = {};   // D2H copy streams (one per sub-batch)
+  cudaStream_t cs = nullptr;           // H2D copy stream (chunk staging)
   cudaStream_t q[2 * kMaxStreams + 1] = {};  // compute streams, descending priority
-  cudaEvent_t staged = nullptr, ls_done[kMaxStreams] = {};
+  // per io slot: its inputs landed (cs), the batch reading them finished (s0),
+  // sub-batch j's signatures copied out (ls[j])
+  cudaEvent_t h2d_done[kSlots] = {}, compute_done[kSlots] = {}, d2h_done[kSlots][kMaxStreams] = {};
   cudaEvent_t done[kMaxStreams] = {}, joins[kMaxStreams] = {}, fjoin[kMaxStreams] = {}, sh_done = nullptr;
   int last_T = 1;
   // host-side cost of each cudaGraphLaunch since the last hs_launch_stats reset
@@ -296,21 +310,23 @@ int check_layout(hs_t* h, int set, const hs_set_config& c) {
   return HS_OK;
 }
 
-int ensure_capacity(hs_t* h, int set, uint32_t count, size_t msg_bytes) {
+int ensure_capacity(hs_t* h, int set, int slot, uint32_t count, size_t msg_bytes) {
   const SetInfo& I = kInfo[set];
   Buffers& B = h->buf[set];
-  void* before[10] = {B.msgs, B.offs, B.keyidx, B.optrand, B.sigs, B.plans, B.idx, B.roots, B.froots, B.stash};
-  CUDA_TRY(h, grow(B.msgs, B.msgs_cap, std::max(msg_bytes, (size_t)1)));
-  CUDA_TRY(h, grow(B.offs, B.offs_cap, (size_t)count + 1));
-  CUDA_TRY(h, grow(B.keyidx, B.keyidx_cap, (size_t)count));
-  CUDA_TRY(h, grow(B.optrand, B.optrand_cap, (size_t)count * I.n));
-  CUDA_TRY(h, grow(B.sigs, B.sigs_cap, (size_t)count * I.sig_bytes));
+  Slot& S = B.io[slot];
+  void* before[11] = {S.msgs, S.offs, S.keyidx, S.optrand, S.sigs, S.wsteps, B.plans, B.idx, B.roots, B.froots, B.stash};
+  CUDA_TRY(h, grow(S.msgs, S.msgs_cap, std::max(msg_bytes, (size_t)1)));
+  CUDA_TRY(h, grow(S.offs, S.offs_cap, (size_t)count + 1));
+  CUDA_TRY(h, grow(S.keyidx, S.keyidx_cap, (size_t)count));
+  CUDA_TRY(h, grow(S.optrand, S.optrand_cap, (size_t)count * I.n));
+  CUDA_TRY(h, grow(S.sigs, S.sigs_cap, (size_t)count * I.sig_bytes));
+  CUDA_TRY(h, grow(S.wsteps, S.wsteps_cap, (size_t)count));
   CUDA_TRY(h, grow(B.plans, B.plans_cap, (size_t)count));
   CUDA_TRY(h, grow(B.idx, B.idx_cap, (size_t)count * I.k));
   CUDA_TRY(h, grow(B.roots, B.roots_cap, (size_t)count * (I.d + 1) * 8));
   CUDA_TRY(h, grow(B.froots, B.froots_cap, (size_t)count * I.k * 8));
   if (h->sets[set].cfg.wots_from_tree) CUDA_TRY(h, grow(B.stash, B.stash_cap, (size_t)count * stash_words(set)));
-  void* after[10] = {B.msgs, B.offs, B.keyidx, B.optrand, B.sigs, B.plans, B.idx, B.roots, B.froots, B.stash};
+  void* after[11] = {S.msgs, S.offs, S.keyidx, S.optrand, S.sigs, S.wsteps, B.plans, B.idx, B.roots, B.froots, B.stash};
   if (std::memcmp(before, after, sizeof before) != 0) {
     B.gen++;
     drop_graphs(h);
@@ -353,16 +369,18 @@ LaunchArgs make_args(hs_t* h, int set, uint32_t first, uint32_t count) {
   const SetInfo& I = kInfo[set];
   SetState& St = h->sets[set];
   Buffers& B = h->buf[set];
+  const Slot& S = B.io[St.slot];
   LaunchArgs a;
   std::memset(&a, 0, sizeof a);
   a.keys = St.keys;
   a.nkeys = St.nkeys;
-  a.msgs = B.msgs;
-  a.offs = B.offs + first;
-  a.key_idx = St.has_keyidx ? B.keyidx + first : nullptr;
-  a.opt_rand = St.has_optrand ? B.optrand + (size_t)first * I.n : nullptr;
+  a.msgs = S.msgs;
+  a.offs = S.offs + first;
+  a.key_idx = St.has_keyidx ? S.keyidx + first : nullptr;
+  a.opt_rand = St.has_optrand ? S.optrand + (size_t)first * I.n : nullptr;
   a.count = count;
-  a.sigs = B.sigs + (size_t)first * I.sig_bytes;
+  a.sigs = S.sigs + (size_t)first * I.sig_bytes;
+  a.wots_steps = S.wsteps ? S.wsteps + first : nullptr;
   a.plans = B.plans + first;
   a.indices = B.idx + (size_t)first * I.k;
   a.roots = B.roots + (size_t)first * (I.d + 1) * 8;
@@ -464,6 +482,7 @@ cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool se
 #define TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
   int kernels = 2;  // msg_prep + WOTS; the shared / FORS / TREE branches are counted by enqueue_*
   TRY(rec(0, h->s0));
+  if (a.wots_steps) TRY(cudaMemsetAsync(a.wots_steps, 0, (size_t)a.count * 4, h->s0));
   if (a.shared_layers > 0)
     TRY(cudaMemsetAsync(a.key_used, 0, used_flag_bytes(set, a.nkeys, a.shared_layers), h->s0));
   TRY(launch(set, K_PREP, c.variant[3], a, h->s0));
@@ -548,6 +567,7 @@ cudaError_t enqueue_batch(hs_t* h, int set, uint32_t count, int T, bool capture)
   int kernels = 0;
 #define TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
   TRY(rec(h->ev[0], h->s0));
+  if (all.wots_steps) TRY(cudaMemsetAsync(all.wots_steps, 0, (size_t)count * 4, h->s0));
   if (all.shared_layers > 0)
     TRY(cudaMemsetAsync(all.key_used, 0, used_flag_bytes(set, all.nkeys, all.shared_layers), h->s0));
   TRY(launch(set, K_PREP, c.variant[3], all, h->s0));
@@ -588,17 +608,30 @@ cudaError_t enqueue_batch(hs_t* h, int set, uint32_t count, int T, bool capture)
   return cudaSuccess;
 }
 
-int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nullptr) {
+// Sign the staged batch (io slot St.slot).  With fetch_to, sub-batch j's
+// signatures (and WOTS step counts, with wsteps_to) are copied to the host on
+// ls[j] as soon as that sub-batch completes; d2h_done[slot][j] marks the copy.
+// Nothing here waits for those copies: the next batch that reuses the slot
+// does (double-buffered chunks in hs_sign_batch).
+int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nullptr, uint32_t* wsteps_to = nullptr,
+              int* T_out = nullptr) {
   if (count == 0) return HS_OK;
   SetState& St = h->sets[set];
   h->last_set = set;
   h->last_mode = mode;
+  const int slot = St.slot;
+  Slot& S = h->buf[set].io[slot];
   const size_t sb = (size_t)kInfo[set].sig_bytes;
   if (int rc = ensure_scratch(h, set, std::max(count, St.staged)); rc != HS_OK) return rc;
+  // inputs of this slot landed; earlier copies out of this slot's signatures finished
+  CUDA_TRY(h, cudaStreamWaitEvent(h->s0, h->h2d_done[slot], 0));
+  for (int j = 0; j < kMaxStreams; j++) CUDA_TRY(h, cudaStreamWaitEvent(h->s0, h->d2h_done[slot][j], 0));
   if (mode == 1) {  // serialised kernels with per-kernel events (roofline timing)
     CUDA_TRY(h, enqueue(h, set, make_args(h, set, 0, count), false, true));
-    if (fetch_to)
-      CUDA_TRY(h, cudaMemcpyAsync(fetch_to, h->buf[set].sigs, count * sb, cudaMemcpyDeviceToHost, h->s0));
+    CUDA_TRY(h, cudaEventRecord(h->compute_done[slot], h->s0));
+    if (fetch_to) CUDA_TRY(h, cudaMemcpyAsync(fetch_to, S.sigs, count * sb, cudaMemcpyDeviceToHost, h->s0));
+    if (wsteps_to) CUDA_TRY(h, cudaMemcpyAsync(wsteps_to, S.wsteps, count * 4, cudaMemcpyDeviceToHost, h->s0));
+    if (T_out) *T_out = 0;
     return HS_OK;
   }
   int T = std::max(1, std::min(St.cfg.streams, kMaxStreams));
@@ -607,7 +640,7 @@ int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nu
   if (St.cfg.use_graph) {
     GraphKey key{set, count, St.has_keyidx ? 1 : 0, St.has_optrand ? 1 : 0, h->buf[set].gen,
                  cfg_fingerprint(St.cfg) + "/" + std::to_string((uintptr_t)St.keys) + "/" + std::to_string(St.nkeys) +
-                     "/L" + std::to_string(St.shared_eff) + "/T" + std::to_string(T)};
+                     "/L" + std::to_string(St.shared_eff) + "/T" + std::to_string(T) + "/S" + std::to_string(slot)};
     auto it = h->graphs.find(key);
     if (it == h->graphs.end()) {
       // bounded cache: a caller that keeps changing batch shapes or configs
@@ -638,48 +671,68 @@ int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nu
   } else {
     CUDA_TRY(h, enqueue_batch(h, set, count, T, false));
   }
-  if (fetch_to) {
+  CUDA_TRY(h, cudaEventRecord(h->compute_done[slot], h->s0));
+  if (fetch_to || wsteps_to) {
     for (int j = 0; j < T; j++) {
       uint32_t first, cn;
       sub_range(count, T, j, first, cn);
       if (cn == 0) break;
       CUDA_TRY(h, cudaStreamWaitEvent(h->ls[j], h->done[j], 0));
-      CUDA_TRY(h, cudaMemcpyAsync(fetch_to + first * sb, h->buf[set].sigs + first * sb, cn * sb,
-                                  cudaMemcpyDeviceToHost, h->ls[j]));
-      CUDA_TRY(h, cudaEventRecord(h->ls_done[j], h->ls[j]));
-      CUDA_TRY(h, cudaStreamWaitEvent(h->s0, h->ls_done[j], 0));
+      if (fetch_to)
+        CUDA_TRY(h, cudaMemcpyAsync(fetch_to + first * sb, S.sigs + first * sb, cn * sb, cudaMemcpyDeviceToHost,
+                                    h->ls[j]));
+      if (wsteps_to)
+        CUDA_TRY(h, cudaMemcpyAsync(wsteps_to + first, S.wsteps + first, (size_t)cn * 4, cudaMemcpyDeviceToHost,
+                                    h->ls[j]));
+      CUDA_TRY(h, cudaEventRecord(h->d2h_done[slot][j], h->ls[j]));
     }
   }
+  if (T_out) *T_out = T;
   return HS_OK;
 }
 
-int stage_inputs(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, const uint32_t* key_idx,
-                 const uint8_t* opt_rand, uint32_t first, uint32_t count) {
+// Stage messages [first, first + count) of the caller's arrays into io slot
+// `slot`: rebased offsets (and the messages unless the caller's buffer is
+// pinned) go through the slot's pinned staging, every H2D runs on the copy
+// stream after the batch that last read the slot, and h2d_done[slot] gates the
+// next run.  Validation happens before anything is copied.
+int stage_inputs(hs_t* h, int set, int slot, const uint8_t* msgs, const uint64_t* offs, const uint32_t* key_idx,
+                 const uint8_t* opt_rand, uint32_t first, uint32_t count, bool msgs_pinned) {
   const SetInfo& I = kInfo[set];
   SetState& St = h->sets[set];
   Buffers& B = h->buf[set];
-  const uint64_t base = offs[first];
-  const uint64_t bytes = offs[first + count] - base;
-  int rc = ensure_capacity(h, set, count, (size_t)bytes);
-  if (rc) return rc;
-  CUDA_TRY(h, grow_host(B.h_offs, B.h_offs_cap, (size_t)count + 1));
-  CUDA_TRY(h, grow_host(B.h_msgs, B.h_msgs_cap, std::max((size_t)bytes, (size_t)1)));
-  for (uint32_t i = 0; i <= count; i++) B.h_offs[i] = offs[first + i] - base;
-  if (bytes) std::memcpy(B.h_msgs, msgs + base, (size_t)bytes);
-  CUDA_TRY(h, cudaMemcpyAsync(B.offs, B.h_offs, ((size_t)count + 1) * 8, cudaMemcpyHostToDevice, h->s0));
-  if (bytes) CUDA_TRY(h, cudaMemcpyAsync(B.msgs, B.h_msgs, (size_t)bytes, cudaMemcpyHostToDevice, h->s0));
-  St.has_keyidx = key_idx != nullptr;
-  St.has_optrand = opt_rand != nullptr;
+  Slot& S = B.io[slot];
   if (key_idx) {
     for (uint32_t i = 0; i < count; i++)
       if (key_idx[first + i] >= St.nkeys)
         return fail(h, HS_E_USAGE, "key_idx[%u]=%u outside the uploaded key table (%u keys)", first + i,
                     key_idx[first + i], St.nkeys);
-    CUDA_TRY(h, cudaMemcpyAsync(B.keyidx, key_idx + first, (size_t)count * 4, cudaMemcpyHostToDevice, h->s0));
   }
+  const uint64_t base = offs[first];
+  const uint64_t bytes = offs[first + count] - base;
+  int rc = ensure_capacity(h, set, slot, count, (size_t)bytes);
+  if (rc) return rc;
+  // the slot's pinned staging is free once its previous H2D finished
+  CUDA_TRY(h, cudaEventSynchronize(h->h2d_done[slot]));
+  CUDA_TRY(h, grow_host(S.h_offs, S.h_offs_cap, (size_t)count + 1));
+  for (uint32_t i = 0; i <= count; i++) S.h_offs[i] = offs[first + i] - base;
+  const uint8_t* msrc = msgs + base;
+  if (bytes && !msgs_pinned) {
+    CUDA_TRY(h, grow_host(S.h_msgs, S.h_msgs_cap, (size_t)bytes));
+    std::memcpy(S.h_msgs, msgs + base, (size_t)bytes);
+    msrc = S.h_msgs;
+  }
+  CUDA_TRY(h, cudaStreamWaitEvent(h->cs, h->compute_done[slot], 0));
+  CUDA_TRY(h, cudaMemcpyAsync(S.offs, S.h_offs, ((size_t)count + 1) * 8, cudaMemcpyHostToDevice, h->cs));
+  if (bytes) CUDA_TRY(h, cudaMemcpyAsync(S.msgs, msrc, (size_t)bytes, cudaMemcpyHostToDevice, h->cs));
+  if (key_idx)
+    CUDA_TRY(h, cudaMemcpyAsync(S.keyidx, key_idx + first, (size_t)count * 4, cudaMemcpyHostToDevice, h->cs));
   if (opt_rand)
-    CUDA_TRY(h, cudaMemcpyAsync(B.optrand, opt_rand + (size_t)first * I.n, (size_t)count * I.n,
-                                cudaMemcpyHostToDevice, h->s0));
+    CUDA_TRY(h, cudaMemcpyAsync(S.optrand, opt_rand + (size_t)first * I.n, (size_t)count * I.n,
+                                cudaMemcpyHostToDevice, h->cs));
+  CUDA_TRY(h, cudaEventRecord(h->h2d_done[slot], h->cs));
+  St.has_keyidx = key_idx != nullptr;
+  St.has_optrand = opt_rand != nullptr;
   // Subtree sharing depth for this batch: at most cfg.shared_layers, within
   // the table budget, and (auto policy) only layers with at most twice as many
   // subtrees per key as the key's messages.  Only subtrees some message reads
@@ -718,6 +771,7 @@ int stage_inputs(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, co
       drop_graphs(h);
     }
   }
+  St.slot = slot;
   St.staged = count;
   return HS_OK;
 }
@@ -760,17 +814,21 @@ int hs_open(int device, hs_t** out) {
   for (auto& ev : h->ev) cudaEventCreate(&ev);
   int prio_least = 0, prio_greatest = 0;
   cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest);
+  cudaStreamCreateWithFlags(&h->cs, cudaStreamNonBlocking);
+  for (int sl = 0; sl < kSlots; sl++) {
+    cudaEventCreateWithFlags(&h->h2d_done[sl], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&h->compute_done[sl], cudaEventDisableTiming);
+    for (int j = 0; j < kMaxStreams; j++) cudaEventCreateWithFlags(&h->d2h_done[sl][j], cudaEventDisableTiming);
+  }
   for (int j = 0; j < kMaxStreams; j++) {
     cudaStreamCreateWithFlags(&h->ls[j], cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&h->fjoin[j], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&h->ls_done[j], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->done[j], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->joins[j], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&h->sh_done, cudaEventDisableTiming);
   for (int j = 0; j < 2 * kMaxStreams + 1; j++)
     cudaStreamCreateWithPriority(&h->q[j], cudaStreamNonBlocking, std::min(prio_greatest + j, prio_least));
-  cudaEventCreateWithFlags(&h->staged, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->join, cudaEventDisableTiming);
   for (int s = 0; s < 3; s++) h->sets[s].cfg = default_config(s);
@@ -785,9 +843,12 @@ void hs_close(hs_t* h) {
   drop_graphs(h);
   for (int s = 0; s < 3; s++) {
     Buffers& B = h->buf[s];
-    cudaFree(B.msgs); cudaFree(B.offs); cudaFree(B.keyidx); cudaFree(B.optrand); cudaFree(B.sigs);
+    for (Slot& S : B.io) {
+      cudaFree(S.msgs); cudaFree(S.offs); cudaFree(S.keyidx); cudaFree(S.optrand); cudaFree(S.sigs);
+      cudaFree(S.wsteps);
+      cudaFreeHost(S.h_msgs); cudaFreeHost(S.h_offs); cudaFreeHost(S.h_sigs); cudaFreeHost(S.h_wsteps);
+    }
     cudaFree(B.plans); cudaFree(B.idx); cudaFree(B.roots); cudaFree(B.froots); cudaFree(B.stash);
-    cudaFreeHost(B.h_msgs); cudaFreeHost(B.h_offs); cudaFreeHost(B.h_sigs);
     cudaFree(h->sets[s].keys);
     cudaFree(B.shared);
     cudaFree(B.key_used);
@@ -801,16 +862,20 @@ void hs_close(hs_t* h) {
     cudaFree(h->sets[s].sk_raw);
   }
   if (h->flush) cudaFree(h->flush);
+  for (int sl = 0; sl < kSlots; sl++) {
+    cudaEventDestroy(h->h2d_done[sl]);
+    cudaEventDestroy(h->compute_done[sl]);
+    for (int j = 0; j < kMaxStreams; j++) cudaEventDestroy(h->d2h_done[sl][j]);
+  }
+  cudaStreamDestroy(h->cs);
   for (int j = 0; j < kMaxStreams; j++) {
     cudaStreamDestroy(h->ls[j]);
     cudaEventDestroy(h->fjoin[j]);
-    cudaEventDestroy(h->ls_done[j]);
     cudaEventDestroy(h->done[j]);
     cudaEventDestroy(h->joins[j]);
   }
   cudaEventDestroy(h->sh_done);
   for (int j = 0; j < 2 * kMaxStreams + 1; j++) cudaStreamDestroy(h->q[j]);
-  cudaEventDestroy(h->staged);
   for (auto& ev : h->ev) cudaEventDestroy(ev);
   cudaEventDestroy(h->fork);
   cudaEventDestroy(h->join);
@@ -927,7 +992,7 @@ int hs_stage(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, const 
   for (uint32_t i = 0; i < count; i++)
     if (offs[i + 1] < offs[i]) return fail(h, HS_E_USAGE, "offsets must be non-decreasing");
   CUDA_TRY(h, cudaSetDevice(h->device));
-  return stage_inputs(h, set, msgs, offs, key_idx, opt_rand, 0, count);
+  return stage_inputs(h, set, 0, msgs, offs, key_idx, opt_rand, 0, count, msgs && is_pinned(msgs));
 }
 
 int hs_run(hs_t* h, int set, uint32_t count, int mode) {
@@ -942,6 +1007,8 @@ int hs_sync(hs_t* h) {
   CUDA_TRY(h, cudaSetDevice(h->device));
   CUDA_TRY(h, cudaStreamSynchronize(h->s0));
   CUDA_TRY(h, cudaStreamSynchronize(h->s1));
+  CUDA_TRY(h, cudaStreamSynchronize(h->cs));
+  for (int j = 0; j < kMaxStreams; j++) CUDA_TRY(h, cudaStreamSynchronize(h->ls[j]));
   return HS_OK;
 }
 
@@ -950,13 +1017,25 @@ int hs_fetch(hs_t* h, int set, uint32_t first, uint32_t count, uint8_t* sigs) {
   if ((uint64_t)first + count > h->sets[set].staged) return fail(h, HS_E_USAGE, "range exceeds the staged batch");
   CUDA_TRY(h, cudaSetDevice(h->device));
   const size_t sb = (size_t)kInfo[set].sig_bytes;
-  CUDA_TRY(h, cudaMemcpyAsync(sigs, h->buf[set].sigs + first * sb, count * sb, cudaMemcpyDeviceToHost, h->s0));
+  const Slot& S = h->buf[set].io[h->sets[set].slot];
+  CUDA_TRY(h, cudaMemcpyAsync(sigs, S.sigs + first * sb, count * sb, cudaMemcpyDeviceToHost, h->s0));
   CUDA_TRY(h, cudaStreamSynchronize(h->s0));
   return HS_OK;
 }
 
 int hs_sign_batch(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, const uint32_t* key_idx,
                   const uint8_t* opt_rand, uint32_t count, uint8_t* sigs) {
+  return hs_sign_batch_ex(h, set, msgs, offs, key_idx, opt_rand, count, sigs, nullptr);
+}
+
+// Chunks of cfg.chunk messages, software-pipelined over two io slots: while
+// chunk c computes (one graph launch on s0), chunk c+1 is staged (host copy +
+// H2D on the copy stream) and chunk c-1's signatures drain to the caller
+// (D2H per sub-batch on ls[j]; straight into the caller's buffer when it is
+// pinned, else through the slot's pinned staging, copied out on the host
+// while the next chunk computes).
+int hs_sign_batch_ex(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, const uint32_t* key_idx,
+                     const uint8_t* opt_rand, uint32_t count, uint8_t* sigs, uint32_t* wots_steps) {
   if (!h || !valid_set(set) || !offs || (count && !sigs)) return fail(h, HS_E_USAGE, "bad arguments");
   if (count == 0) return HS_OK;
   if (!msgs && offs[count] != offs[0]) return fail(h, HS_E_USAGE, "null message buffer");
@@ -967,24 +1046,49 @@ int hs_sign_batch(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs, c
   const size_t sb = (size_t)kInfo[set].sig_bytes;
   const uint32_t chunk = (uint32_t)std::max(1, h->sets[set].cfg.chunk);
   const bool direct = is_pinned(sigs);
+  const bool wdirect = wots_steps && is_pinned(wots_steps);
+  const bool mpinned = msgs && is_pinned(msgs);
   Buffers& B = h->buf[set];
-  float total_ms = 0.f, part[4] = {0, 0, 0, 0};
-  for (uint32_t first = 0; first < count; first += chunk) {
+  struct Pending {
+    int slot = -1, T = 0;
+    uint32_t first = 0, cn = 0;
+  } prev;
+  // a chunk's host-side tail: wait for its copies, move staged bytes out
+  auto drain = [&](const Pending& pc) -> int {
+    if (pc.slot < 0) return HS_OK;
+    for (int j = 0; j < std::max(pc.T, 1); j++) CUDA_TRY(h, cudaEventSynchronize(h->d2h_done[pc.slot][j]));
+    if (pc.T == 0) CUDA_TRY(h, cudaStreamSynchronize(h->s0));  // serial mode copies on s0
+    const Slot& S = B.io[pc.slot];
+    if (!direct) std::memcpy(sigs + pc.first * sb, S.h_sigs, pc.cn * sb);
+    if (wots_steps && !wdirect) std::memcpy(wots_steps + pc.first, S.h_wsteps, (size_t)pc.cn * 4);
+    return HS_OK;
+  };
+  int rc = HS_OK;
+  uint32_t c = 0;
+  for (uint32_t first = 0; first < count && rc == HS_OK; first += chunk, c++) {
     const uint32_t cn = std::min(chunk, count - first);
-    int rc = stage_inputs(h, set, msgs, offs, key_idx, opt_rand, first, cn);
-    if (rc) return rc;
-    if (!direct) CUDA_TRY(h, grow_host(B.h_sigs, B.h_sigs_cap, (size_t)cn * sb));
-    rc = run_batch(h, set, cn, 0, direct ? sigs + first * sb : B.h_sigs);
-    if (rc) return rc;
-    CUDA_TRY(h, cudaStreamSynchronize(h->s0));
-    if (!direct) std::memcpy(sigs + first * sb, B.h_sigs, cn * sb);
-    float ms[5];
-    if (hs_timings(h, ms, 5) == 5) {
-      total_ms += ms[0];
-      for (int i = 0; i < 4; i++) part[i] += ms[1 + i];
-    }
+    const int slot = (int)(c & 1u);
+    rc = stage_inputs(h, set, slot, msgs, offs, key_idx, opt_rand, first, cn, mpinned);
+    if (rc) break;
+    Slot& S = B.io[slot];
+    // the slot's pinned output staging was drained by the previous iteration
+    if (!direct) CUDA_TRY(h, grow_host(S.h_sigs, S.h_sigs_cap, (size_t)cn * sb));
+    if (wots_steps && !wdirect) CUDA_TRY(h, grow_host(S.h_wsteps, S.h_wsteps_cap, (size_t)cn));
+    int T = 0;
+    rc = run_batch(h, set, cn, 0, direct ? sigs + first * sb : S.h_sigs,
+                   wots_steps ? (wdirect ? wots_steps + first : S.h_wsteps) : nullptr, &T);
+    if (rc) break;
+    if (int r2 = drain(prev); r2 != HS_OK) return r2;
+    prev = Pending{slot, T, first, cn};
   }
-  return HS_OK;
+  if (rc == HS_OK) rc = drain(prev);
+  cudaError_t e = cudaStreamSynchronize(h->s0);
+  if (rc == HS_OK && e != cudaSuccess) rc = fail(h, HS_E_CUDA, "sign: %s", cudaGetErrorString(e));
+  for (int j = 0; j < kMaxStreams; j++) {
+    e = cudaStreamSynchronize(h->ls[j]);
+    if (rc == HS_OK && e != cudaSuccess) rc = fail(h, HS_E_CUDA, "sign copy-out: %s", cudaGetErrorString(e));
+  }
+  return rc;
 }
 
 int hs_verify_batch(hs_t* h, int set, const uint8_t* pks, uint32_t nkeys, const uint8_t* msgs, const uint64_t* offs,

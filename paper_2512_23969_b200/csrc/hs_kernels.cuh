@@ -93,6 +93,10 @@ struct LaunchArgs {
   uint32_t* chain_ends;
   uint32_t* shared_ends;     // split shared subtrees: [key][unit][leaf][chain][NW] (nullable)
   uint32_t* fors_lpre;       // [msg][log_t + 1][8]: per FORS level the H state after ADRS rounds 0..4
+  // WOTS_Sign F steps per message (sum of the signed base-w digits over all
+  // d layers; zeroed before the batch), for the exact compression count the
+  // reference's ctx_out reports (hashes.py:117-159).  nullable.
+  uint32_t* wots_steps;
 };
 
 __device__ __forceinline__ uint64_t shr64(uint64_t x, int s) { return s >= 64 ? 0ull : (x >> s); }
@@ -1077,6 +1081,15 @@ __device__ __forceinline__ uint32_t wots_digit(const uint32_t* msg_w, int chain)
   return (csum >> (12 - 4 * c)) & 15u;
 }
 
+// ctr[msg] += v over the calling threads, one atomic per distinct msg in the
+// warp (threads of a message are contiguous in the WOTS grids).
+__device__ __forceinline__ void add_per_message(uint32_t* ctr, uint32_t msg, uint32_t v) {
+  const unsigned active = __activemask();
+  const unsigned peers = __match_any_sync(active, msg);
+  const uint32_t sum = __reduce_add_sync(peers, v);
+  if ((int)(threadIdx.x & 31u) == __ffs(peers) - 1) atomicAdd(ctr + msg, sum);
+}
+
 template <int S, class V>
 __global__ void __launch_bounds__(kSmallBlock) wots_sign_kernel(LaunchArgs a) {
   using Pr = P<S>;
@@ -1112,6 +1125,7 @@ __global__ void __launch_bounds__(kSmallBlock) wots_sign_kernel(LaunchArgs a) {
   chain_F<V, NW>(x, mid, wa, 0u, digit);
   store_node<NW>(a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_ht + (size_t)layer * Pr::layer_bytes + chain * Pr::n,
                  x);
+  if (a.wots_steps) add_per_message(a.wots_steps, msg, digit);
 }
 
 // WOTS+_Sign as a gather: TREE_Sign already walked every chain of each
@@ -1168,6 +1182,7 @@ __global__ void __launch_bounds__(kSmallBlock) wots_gather_kernel(LaunchArgs a) 
 #pragma unroll
   for (int j = 0; j < NW; j++) x[j] = src[j];
   store_node<NW>(lsig + chain * Pr::n, x);
+  if (a.wots_steps) add_per_message(a.wots_steps, msg, digit);
 }
 
 // ---------------------------------------------------------------------------

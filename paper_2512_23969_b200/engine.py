@@ -194,30 +194,40 @@ class Engine:
 
     # -- signing ---------------------------------------------------------
     def sign_into(self, set_id: str, blob, offs: np.ndarray, count: int, out, key_idx: np.ndarray | None = None,
-                  opt_rand=None) -> None:
-        """Zero-copy batch sign: inputs/outputs are caller buffers (pinned ones avoid staging)."""
+                  opt_rand=None, wots_steps=None) -> None:
+        """Zero-copy batch sign: inputs/outputs are caller buffers (pinned ones avoid staging).
+        ``wots_steps`` (a uint32 array of ``count``, or a pointer) receives each
+        message's WOTS_Sign F steps -- the data-dependent term of the exact
+        compression count (hs_sign_batch_ex)."""
         p = derive(set_id)
         offs = _offsets(offs, count)
         key_idx = _key_index(key_idx, count)
         if opt_rand is not None and not isinstance(opt_rand, int) and len(opt_rand) < count * p.n:
             raise UsageError(f"opt_rand must be {p.n} bytes per message")
+        if isinstance(wots_steps, np.ndarray) and (wots_steps.dtype != np.uint32 or wots_steps.size < count
+                                                    or not wots_steps.flags.c_contiguous):
+            raise UsageError(f"wots_steps must be a contiguous uint32 array of {count}")
         with self._lock:
             self._check(
-                _lib.lib().hs_sign_batch(self._h, p.index, _u8ptr(blob), _u8ptr(offs),
-                                         _u8ptr(key_idx) if key_idx is not None else None, _u8ptr(opt_rand),
-                                         count, _u8ptr(out)),
-                "hs_sign_batch")
+                _lib.lib().hs_sign_batch_ex(self._h, p.index, _u8ptr(blob), _u8ptr(offs),
+                                            _u8ptr(key_idx) if key_idx is not None else None, _u8ptr(opt_rand),
+                                            count, _u8ptr(out), _u8ptr(wots_steps)),
+                "hs_sign_batch_ex")
 
     def sign_batch(self, set_id: str, msgs: Sequence[bytes], key_idx: Sequence[int] | None = None,
-                   opt_rand: Sequence[bytes] | bytes | None = None) -> list[bytes]:
+                   opt_rand: Sequence[bytes] | bytes | None = None, counts: bool = False):
+        """Sign a list of messages; with ``counts`` also return each message's
+        WOTS_Sign F steps (``(sigs, steps)``)."""
         p = derive(set_id)
         count = len(msgs)
         with self._lock:
             if set_id not in self._keys:
                 raise UsageError("no keys uploaded for this parameter set")
-            return self._sign_batch(p, set_id, msgs, count, key_idx, opt_rand) if count else []
+            if not count:
+                return ([], []) if counts else []
+            return self._sign_batch(p, set_id, msgs, count, key_idx, opt_rand, counts)
 
-    def _sign_batch(self, p, set_id, msgs, count, key_idx, opt_rand) -> list[bytes]:
+    def _sign_batch(self, p, set_id, msgs, count, key_idx, opt_rand, counts):
         blob, offs = pack_messages(msgs)
         kidx = None
         if key_idx is not None:
@@ -239,9 +249,11 @@ class Engine:
                 raise UsageError(f"opt_rand must be {p.n} bytes per message")
             orand = bytes(orand)
         out = bytearray(count * p.sig_bytes)
-        self.sign_into(set_id, blob, offs, count, out, kidx, orand)
+        steps = np.zeros(count, dtype=np.uint32) if counts else None
+        self.sign_into(set_id, blob, offs, count, out, kidx, orand, steps)
         sb = p.sig_bytes
-        return [bytes(out[i * sb:(i + 1) * sb]) for i in range(count)]
+        sigs = [bytes(out[i * sb:(i + 1) * sb]) for i in range(count)]
+        return (sigs, [int(x) for x in steps]) if counts else sigs
 
     def verify_batch(self, set_id: str, pks: Sequence[bytes] | bytes, msgs: Sequence[bytes], sigs: Sequence[bytes],
                      key_idx: Sequence[int] | None = None) -> list[bool]:

@@ -63,16 +63,20 @@ class SecretKey:
 
 
 class SignContext:
-    """Stand-in for the reference's HashContext handed out via ``ctx_out``.
+    """Stand-in for the reference's HashContext handed out via ``ctx_out``
+    (sigcore.py:166-168).
 
-    ``compressions`` is the closed-form count of the work one signature
-    represents (params.compressions_per_signature), with the WOTS_Sign term
-    at its expectation.
+    ``compressions`` is the exact SHA-256 compression count the reference's
+    default path records for this signature (hashes.py:117-159): the fixed
+    per-stage terms of params.compressions_per_signature plus ``wots_steps``,
+    the WOTS_Sign F steps the device counted while signing (the sum of the
+    signed base-w digits over all layers).
     """
 
-    def __init__(self, p: DerivedParams, msg_len: int):
+    def __init__(self, p: DerivedParams, msg_len: int, wots_steps: int):
         self.params = p
-        self.compressions = int(round(compressions_per_signature(p, msg_len)["total"]))
+        self.wots_steps = int(wots_steps)
+        self.compressions = int(compressions_per_signature(p, msg_len, digit_sum=self.wots_steps)["total"])
 
 
 def _sk_of(sk) -> SecretKey:
@@ -163,6 +167,25 @@ def sign_batch(
 ) -> list[bytes]:
     """Sign a batch in one graph launch.  ``sk`` is one SecretKey or a list
     (then ``key_idx[i]`` picks message i's key; default key 0)."""
+    return sign_on_engine(get_engine(), msgs, sk, params, key_idx=key_idx, opt_rand=opt_rand, fusion=fusion,
+                          relax=relax, selection=selection, ctx_out=ctx_out)
+
+
+def sign_on_engine(
+    eng,
+    msgs: Sequence[bytes],
+    sk,
+    params: DerivedParams | str,
+    *,
+    key_idx: Sequence[int] | None = None,
+    opt_rand: Sequence[bytes] | None = None,
+    fusion=None,
+    relax=None,
+    selection=None,
+    ctx_out: list | None = None,
+) -> list[bytes]:
+    """``sign_batch`` on a given engine (an ``Engine``, or any object with its
+    lock / upload_keys / config / set_config / sign_batch methods)."""
     p = derive(params)
     keys = [_sk_of(k) for k in (sk if isinstance(sk, (list, tuple)) else [sk])]
     if not keys:
@@ -180,7 +203,6 @@ def sign_batch(
         if any(o is None for o in opt_rand):
             kk = list(key_idx) if key_idx is not None else [0] * len(msgs)
             opt_rand = [o if o is not None else keys[kk[i]].pk_seed for i, o in enumerate(opt_rand)]
-    eng = get_engine()
     # the engine is process-wide: key table, per-call overrides, the sign and
     # the restore form one critical section, so concurrent callers (threads,
     # several GraphSigners) never sign under each other's keys or layout
@@ -188,13 +210,16 @@ def sign_batch(
         eng.upload_keys(p.id, [k.to_bytes() for k in keys])
         before = _apply_overrides(eng, p, fusion, relax, selection)
         try:
-            sigs = eng.sign_batch(p.id, [bytes(m) for m in msgs], key_idx=key_idx, opt_rand=opt_rand)
+            res = eng.sign_batch(p.id, [bytes(m) for m in msgs], key_idx=key_idx, opt_rand=opt_rand,
+                                 counts=ctx_out is not None)
         finally:
             if before is not None:
                 eng.set_config(p.id, **before)
-    if ctx_out is not None:
-        for m in msgs:
-            ctx_out.append(SignContext(p, len(m)))
+    if ctx_out is None:
+        return res
+    sigs, steps = res
+    for m, st in zip(msgs, steps):
+        ctx_out.append(SignContext(p, len(m), st))
     return sigs
 
 

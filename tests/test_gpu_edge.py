@@ -5,12 +5,13 @@ from __future__ import annotations
 
 import random
 
+import numpy as np
 import pytest
 
 from conftest import SETS
 
 import paper_2512_23969_b200 as hs
-from paper_2512_23969_b200.params import derive
+from paper_2512_23969_b200.params import compressions_per_signature, derive
 
 pytestmark = pytest.mark.gpu
 
@@ -79,14 +80,62 @@ def test_chunked_multistream_mixed_keys(eng, oracle_mod, set_id):
     base = eng.config(set_id)
     try:
         eng.set_config(set_id, chunk=1024, streams=4)
-        sigs = eng.sign_batch(set_id, msgs, key_idx=kidx, opt_rand=opts)
+        sigs, steps = eng.sign_batch(set_id, msgs, key_idx=kidx, opt_rand=opts, counts=True)
     finally:
         eng.set_config(set_id, **base)
     # oracle: opt_rand None means PK.seed (sigcore.py:162-163)
     blob = b"".join(o if o is not None else sks[k][2 * p.n:3 * p.n] for o, k in zip(opts, kidx))
-    ref, _ = oracle_mod.sign_many(set_id, b"".join(sks), kidx, msgs, blob)
+    ref, comps = oracle_mod.sign_many(set_id, b"".join(sks), kidx, msgs, blob)
     bad = [i for i in range(count) if sigs[i] != ref[i]]
     assert not bad, bad[:10]
+    # the per-message WOTS step counts add up to the oracle's compression count
+    # (oracle path = default path + k re-derived FORS secrets, tests/oracle_engine.py)
+    fixed = sum(compressions_per_signature(p, len(m), digit_sum=0)["total"] for m in msgs)
+    assert sum(steps) == comps - count * p.k - fixed
+    assert all(0 <= x <= p.d * p.wots_len * (p.w - 1) for x in steps)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_pipelined_chunks_io(eng, oracle_mod, pinned):
+    """hs_sign_batch_ex's two-slot pipeline over 4 chunks (the last one ragged),
+    with pinned or pageable message / signature / step-count buffers: the bytes
+    and counts equal a single-chunk run, and sampled signatures the oracle's."""
+    from paper_2512_23969_b200.engine import PinnedBuffer, pack_messages
+
+    set_id = "192f"
+    p = derive(set_id)
+    rng = random.Random(99)
+    sks = [oracle_mod.keygen(set_id, rng.randbytes(3 * p.n)) for _ in range(3)]
+    count = 1000
+    msgs = [rng.randbytes(rng.choice([1, 32, 90])) for _ in range(count)]
+    kidx = np.array([rng.randrange(3) for _ in range(count)], dtype=np.uint32)
+    eng.upload_keys(set_id, sks)
+    blob, offs = pack_messages(msgs)
+    base = eng.config(set_id)
+    bufs = []
+    try:
+        eng.set_config(set_id, chunk=count)
+        one, one_steps = eng.sign_batch(set_id, msgs, key_idx=kidx, counts=True)
+        eng.set_config(set_id, chunk=300, streams=3)
+        if pinned:
+            mb, ob, sb = PinnedBuffer(len(blob)), PinnedBuffer(count * p.sig_bytes), PinnedBuffer(4 * count)
+            bufs = [mb, ob, sb]
+            mb.array()[:] = np.frombuffer(blob, dtype=np.uint8)
+            eng.sign_into(set_id, mb.ptr, offs, count, ob.ptr, kidx, None, sb.ptr)
+            raw, steps = bytes(ob.view), [int(x) for x in sb.array(np.uint32)]
+        else:
+            out, st = bytearray(count * p.sig_bytes), np.zeros(count, dtype=np.uint32)
+            eng.sign_into(set_id, blob, offs, count, out, kidx, None, st)
+            raw, steps = bytes(out), [int(x) for x in st]
+    finally:
+        eng.set_config(set_id, **base)
+        for b in bufs:
+            b.free()
+    sigs = [raw[i * p.sig_bytes:(i + 1) * p.sig_bytes] for i in range(count)]
+    assert sigs == one and steps == one_steps
+    check = [0, 299, 300, 599, 600, 899, 900, 999]
+    ref, _ = oracle_mod.sign_many(set_id, b"".join(sks), [int(kidx[i]) for i in check], [msgs[i] for i in check])
+    assert [sigs[i] for i in check] == ref
 
 
 def test_verify_into_pinned_roundtrip(eng, oracle_mod):

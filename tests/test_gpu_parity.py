@@ -38,7 +38,10 @@ def test_sign_golden(eng, golden, set_id):
     for case in g["sign"]:
         sk = hs.SecretKey.from_bytes(H(case["sk"]), p)
         opt = H(case["opt_rand"]) if case["opt_rand"] else None
-        sig = hs.sign(H(case["msg"]), sk, p, opt_rand=opt)
+        ctx = []
+        sig = hs.sign(H(case["msg"]), sk, p, opt_rand=opt, ctx_out=ctx)
+        # ctx_out carries the reference's exact HashContext count (sigcore.py:166-168)
+        assert ctx[0].compressions == case["compressions"], case["tag"]
         if case["tag"] == "zero":
             ref = (GOLDEN_DIR / f"sig_{set_id}_zero.bin").read_bytes()
             if sig != ref:
@@ -228,22 +231,27 @@ def test_config2_full_batch_128f(eng, config2, streams):
 
 
 def test_graph_signer_stage_plugin(eng, oracle_mod):
-    """The reference's stage-plugin protocol (batchgraph.py:93-131, 245-353) driven by
-    the task-graph scheduler: one GPU batch per instantiated graph set, bytes == oracle."""
-    from paper_2512_23969_b200 import batchgraph as bg
+    """The reference's stage-plugin protocol (batchgraph.py:93-131, 245-353) driven
+    with random stage orders on 4 threads (tests/stage_driver.py; the reference's
+    own scheduler runs the same plugin on CPU in test_tuner_config_graph.py): one
+    GPU batch for all prepared messages, bytes == oracle, exact compression count."""
+    from oracle_engine import oracle_wots_steps
+    from stage_driver import drive, order_ok
+
+    from paper_2512_23969_b200.batchgraph import GraphSigner
 
     p = derive("128f")
     rng = random.Random(11)
     sk_raw = oracle_mod.keygen("128f", rng.randbytes(48))
     sk = hs.SecretKey.from_bytes(sk_raw, p)
     msgs = [rng.randbytes(rng.choice([0, 32, 77])) for _ in range(24)]
-    signer = bg.GraphSigner(sk, p)
-    graphs = bg.build_graphs(msgs, m=8, T=3)
-    pool = bg.BufferPool()
-    sigs, log = bg.execute_graphs(graphs, 4, signer, pool=pool, rng=random.Random(3))
-    assert bg.replay_check(log, graphs)
-    assert signer.launches == 1 and pool.allocations == len(msgs)
+    signer = GraphSigner(sk, p, engine=eng)
+    sigs, log = drive(signer, msgs, workers=4, seed=3)
+    assert order_ok(log, len(msgs))
+    assert signer.launches == 1
     assert sigs == [oracle_mod.sign("128f", sk_raw, m) for m in msgs]
+    assert signer.compressions == sum(hs.compressions_per_signature(
+        p, len(m), digit_sum=oracle_wots_steps(oracle_mod, "128f", sk_raw, m))["total"] for m in msgs)
 
 
 def test_config_apply_roundtrip(eng, tmp_path):

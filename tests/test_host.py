@@ -3,6 +3,7 @@
 from __future__ import annotations
 
 import ctypes
+import hashlib
 import os
 import re
 from pathlib import Path
@@ -145,3 +146,37 @@ def test_compiled_sha_paths(L):
     if not os.environ.get("HERO_SIGN_LIB"):
         assert names[2:] == tuple(f"mx{m & 255}" + (f"p{m >> 8}" if m >> 8 else "") for m in masks)
     assert all(re.fullmatch(r"mx\d+(p\d+)?", n) for n in names[2:])
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_oracle_wots_steps_pinned(golden, oracle_mod, set_id):
+    """The oracle's compression counter minus its k re-derived FORS secrets is the
+    reference's default-path count (hashes.py:117-159), for every golden sign
+    case: this pins the per-message WOTS step counts the tests derive from it."""
+    from oracle_engine import oracle_wots_steps
+
+    p = derive(set_id)
+    for case in golden["sets"][set_id]["sign"]:
+        msg = bytes.fromhex(case["msg"])
+        opt = bytes.fromhex(case["opt_rand"]) if case["opt_rand"] else None
+        steps = oracle_wots_steps(oracle_mod, set_id, bytes.fromhex(case["sk"]), msg, opt)
+        assert compressions_per_signature(p, len(msg), digit_sum=steps)["total"] == case["compressions"]
+
+
+def test_ctx_out_exact_on_engine(golden, oracle_mod):
+    """sigcore's ctx_out path (sign_on_engine) turns the engine's per-message WOTS
+    step counts into SignContext.compressions equal to the reference's count."""
+    from oracle_engine import OracleEngine
+
+    from paper_2512_23969_b200.sigcore import SecretKey, sign_on_engine
+
+    eng = OracleEngine(oracle_mod)
+    for set_id in SETS:
+        p = derive(set_id)
+        for case in golden["sets"][set_id]["sign"]:
+            ctx = []
+            opt = [bytes.fromhex(case["opt_rand"])] if case["opt_rand"] else None
+            sig = sign_on_engine(eng, [bytes.fromhex(case["msg"])], SecretKey.from_bytes(bytes.fromhex(case["sk"]), p),
+                                 p, opt_rand=opt, ctx_out=ctx)[0]
+            assert hashlib.sha256(sig).hexdigest() == case["sig_sha256"]
+            assert ctx[0].compressions == case["compressions"], (set_id, case["tag"])

