@@ -26,9 +26,15 @@ cpu_baseline: the C restatement of the reference signer (oracle/, a "port"),
 launch_latency: the metric's "batch launch latency": host time inside the
          one cudaGraphLaunch per batch, device batch time, public-API wall
          time per batch, and small-batch (1 / 64 message) API latency.
-other_sets: the same measurements for the other two parameter sets (192f and
-         256f at 16384 messages per GPU, 128f at 4096), so one default run
+other_sets: the same measurements for the other two parameter sets at their
+         BASELINE batch sizes (192f: 16384 messages per GPU, configs[2];
+         256f: 65536, configs[3] -- signed as 4 chunk launches of 16384 over
+         resident inputs), each with its own CPU baseline, so one default run
          covers 128f/192f/256f; --single-set skips them.
+--gpus N: one process per GPU.  Under torchrun WORLD_SIZE must equal N;
+         launched plainly with N > 1, bench.py spawns the N ranks itself
+         (RANK / LOCAL_RANK / WORLD_SIZE, rendezvous on 127.0.0.1) and relays
+         rank 0's line; --plan prints that launch plan without running.
 """
 
 from __future__ import annotations
@@ -36,11 +42,13 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import random
+import socket
+import ssl
 import statistics
 import subprocess
 import sys
-import threading
 import time
 from pathlib import Path
 
@@ -64,7 +72,65 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--check", type=int, default=16, help="signatures checked vs the oracle after timing")
     ap.add_argument("--single-set", action="store_true", help="skip the secondary sets (other_sets)")
+    ap.add_argument("--plan", action="store_true", help="print the rank launch plan as JSON and exit")
     return ap.parse_args()
+
+
+# BASELINE.json configs each set's batch size comes from
+BASELINE_CONFIG = {("128f", 4096): "configs[1]", ("192f", 16384): "configs[2]", ("256f", 65536): "configs[3]"}
+
+
+def bench_config(set_id: str, count: int, gpus: int) -> dict:
+    """The workload both arms report (identical dicts, so the driver can match
+    the reference arm's line to ours)."""
+    return {"workload": f"SPHINCS+-{set_id} batched sign, {count} x 32-byte msgs per GPU, 1 key",
+            "set": set_id, "messages_per_gpu": count, "message_bytes": 32, "keys": 1, "global_batch": gpus * count,
+            "parallelism": f"message-shard x{gpus}",
+            "baseline_config": BASELINE_CONFIG.get((set_id, count), "custom")}
+
+
+def host_info() -> dict:
+    """CPU model and the versions BASELINE.md s.3 asks to report beside a CPU baseline."""
+    model = platform.processor() or ""
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "python": platform.python_version(),
+            "openssl": ssl.OPENSSL_VERSION}
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def rank_plan(gpus: int, port: int) -> list[dict]:
+    """Environment of each rank when bench.py launches the N processes itself
+    (the same variables torchrun sets; one process per GPU, LOCAL_RANK picks it)."""
+    return [{"RANK": str(r), "LOCAL_RANK": str(r), "WORLD_SIZE": str(gpus), "LOCAL_WORLD_SIZE": str(gpus),
+             "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)} for r in range(gpus)]
+
+
+def spawn_ranks(gpus: int) -> int:
+    """Run this script once per GPU and relay rank 0's stdout (its JSON line)."""
+    plan = rank_plan(gpus, free_port())
+    procs = []
+    for env in plan:
+        procs.append(subprocess.Popen([sys.executable, str(Path(__file__).resolve())] + sys.argv[1:],
+                                      env=dict(os.environ, **env),
+                                      stdout=subprocess.PIPE if env["RANK"] == "0" else subprocess.DEVNULL))
+    out, _ = procs[0].communicate()
+    rc = max(abs(pr.wait()) for pr in procs)
+    sys.stdout.write(out.decode())
+    sys.stdout.flush()
+    return rc
 
 
 def dist_env():
@@ -182,12 +248,22 @@ def cpu_sign_rate(set_id: str, sk: bytes, msgs: list[bytes], seconds: float, thr
     return n / dt, n, dt
 
 
+def cpu_baseline_line(set_id: str, sk: bytes, msgs: list[bytes], seconds: float) -> dict:
+    """cpu_baseline object: the oracle port on every host thread, a bounded sample."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle  # CPU baseline leg only
+
+    threads = os.cpu_count() or 1
+    rate, n, dt = cpu_sign_rate(set_id, sk, msgs, seconds, threads)
+    return {"value": round(rate, 3), "unit": "sig/s", "cores": threads, "kind": "port",
+            "sample": f"{n} of the same {set_id} messages in {dt:.1f}s, C oracle (oracle/hs_oracle.c, "
+                      f"SHA-NI={oracle.shani_active()})", **host_info()}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from paper_2512_23969_b200.params import derive
-
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle  # reference arm: the CPU restatement of the reference signer
 
@@ -195,7 +271,6 @@ def run_reference(args):
     p, seed, msgs = workload(args.set_id, args.count, 0)
     sk = oracle.keygen(args.set_id, seed)
     threads = os.cpu_count() or 1
-    per_step = max(threads, int(threads * 2))
     rate_probe, _, _ = cpu_sign_rate(args.set_id, sk, msgs, 1.0, threads)
     per_step = int(max(threads, min(args.count, rate_probe * max(1.0, 60.0 / max(1, args.steps + args.warmup)))))
     for _ in range(args.warmup):
@@ -212,11 +287,10 @@ def run_reference(args):
         "unit": "sig/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * statistics.mean(times), 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"SPHINCS+-{args.set_id} sign, {args.count} x 32-byte msgs, 1 key (per-step sample "
-                               f"of {per_step} msgs)", "set": args.set_id},
+        "config": bench_config(args.set_id, args.count, args.gpus),
         "cpu_baseline": {"value": round(value, 3), "unit": "sig/s", "cores": threads, "kind": "port",
-                         "sample": f"{per_step} signatures per step x {args.steps} steps, C oracle "
-                                   f"(oracle/hs_oracle.c, SHA-NI={oracle.shani_active()})"},
+                         "sample": f"{per_step} of the workload's signatures per step x {args.steps} steps, C "
+                                   f"oracle (oracle/hs_oracle.c, SHA-NI={oracle.shani_active()})", **host_info()},
         "e2e": {"value": round(value, 3), "unit": "sig/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -235,11 +309,12 @@ def measure_set(eng, info, set_id: str, count: int, steps: int, warmup: int, ran
     sk = eng.keygen_batch(set_id, [seed])[0]
     eng.upload_keys(set_id, sk)
     blob, offs = pack_messages(msgs)
+    cfg = eng.config(set_id)
+    chunk = min(count, cfg["chunk"])  # messages per graph launch
 
     # ---- value: inputs resident in HBM, device-timed graph launches ----
     eng.stage(set_id, blob, offs, count)
     flush = 256 << 20
-    cfg = eng.config(set_id)
     eng.bench_run(set_id, count, max(1, warmup), 0, flush)
     shape = eng.batch_info(set_id)
     shared_L = shape["shared_layers"]  # depth the auto policy chose for this batch
@@ -266,25 +341,27 @@ def measure_set(eng, info, set_id: str, count: int, steps: int, warmup: int, ran
         plain_s = max_over_ranks(dist, sum(plain_ms) / 1e3)
         value_plain = world * count * steps / plain_s
         eng.set_config(set_id, shared_layers=cfg["shared_layers"])
-        eng.stage(set_id, blob, offs, count)
-        assert eng.batch_info(set_id)["shared_layers"] == shared_L
 
-    # ---- per-kernel roofline (serialised run, CUDA events around each kernel) ----
-    eng.bench_run(set_id, count, 1, 1, flush)
+    # ---- per-kernel roofline (serialised run of one launch's chunk, CUDA events around each kernel) ----
+    rblob, roffs = pack_messages(msgs[:chunk])
+    eng.stage(set_id, rblob, roffs, chunk)
+    eng.bench_run(set_id, chunk, 1, 1, flush)
     kt = [eng.timings()]
     tree_ms = []
     for _ in range(3):
-        eng.bench_run(set_id, count, 1, 1, flush)
+        eng.bench_run(set_id, chunk, 1, 1, flush)
         tree_ms.append(eng.timings()["TREE_Sign"])
     tree_ms_avg = statistics.mean(tree_ms)
+    rinfo = eng.batch_info(set_id)
+    rshared_L = rinfo["shared_layers"]
+    units = rinfo["shared_subtrees_built"]  # shared subtrees the launch actually read
     work = hs.compressions_per_signature(p, 32)
     sub = hs.params.subtree_compressions(p)
-    units = eng.batch_info(set_id)["shared_subtrees_built"]  # shared subtrees the batch actually read
     # executed compressions of the timed per-message TREE_Sign kernel (the
     # subtrees below the shared layers); the shared-subtree kernel (`units`
     # subtrees of the single key, run concurrently in the graph) is counted in
     # executed_per_sig but not in the roofline kernel
-    tree_comps = count * (p.d - shared_L) * sub
+    tree_comps = chunk * (p.d - rshared_L) * sub
     achieved = tree_comps / (tree_ms_avg / 1e3)
     clk = clocks.summary()
     sm_max = clk.get("sm_max_mhz") or 1965.0
@@ -294,11 +371,20 @@ def measure_set(eng, info, set_id: str, count: int, steps: int, warmup: int, ran
     if tpath.exists():
         try:
             traffic = json.loads(tpath.read_text()).get(set_id, {}).get("bytes_per_launch_per_msg")
-            traffic = traffic * count if traffic is not None else None
+            traffic = traffic * chunk if traffic is not None else None
         except (ValueError, AttributeError):
             traffic = None
-    executed_per_sig = (work["host"] + work["FORS_Sign"] + (tree_comps + units * sub) / count
+    executed_per_sig = (work["host"] + work["FORS_Sign"] + (tree_comps + units * sub) / chunk
                         + (0 if cfg["wots_from_tree"] else work["WOTS_Sign"]))
+    per_gpu = value / world
+    step_fracs = {
+        "reference_count": round(per_gpu * work["total"] / peak, 4),
+        "executed_count": round(per_gpu * executed_per_sig / peak, 4),
+        "no_subtree_sharing": round(value_plain / world * work["total"] / peak, 4) if value_plain else None,
+        "note": "whole-step compressions/s per GPU / int-issue peak: at the reference's count per signature "
+                "(what a signature is worth), at the count the kernels execute (subtree sharing computes the "
+                "top layers once per batch), and with sharing off (every message computes every layer)",
+    }
 
     # ---- e2e: public API, pinned host buffers, H2D + sign + D2H every step ----
     h_blob = PinnedBuffer(max(len(blob), 1))
@@ -356,8 +442,9 @@ def measure_set(eng, info, set_id: str, count: int, steps: int, warmup: int, ran
             "e2e_batch_us": round(1e6 * e2e_s / steps, 1),
             "e2e_graph_launches_per_batch": round(e2e_launch["graph_launches"] / max(1, steps), 3),
             "e2e_small_batch_us": small,
-            "note": "host time inside cudaGraphLaunch (one graph per batch); device batch time (CUDA events); "
-                    "public-API wall time per batch incl. H2D/D2H; median wall time of small batches (messages: us)",
+            "note": "host time inside cudaGraphLaunch (one graph per batch of up to `chunk` messages); device "
+                    "batch time (CUDA events); public-API wall time per batch incl. H2D/D2H; median wall time of "
+                    "small batches (messages: us)",
         },
         "roofline": {
             "bound": "int-issue",
@@ -367,11 +454,12 @@ def measure_set(eng, info, set_id: str, count: int, steps: int, warmup: int, ran
             "unit": "Gcompressions/s",
             "frac": round(achieved / peak, 4),
             "traffic": traffic,
-            "work_per_launch": f"{count} msgs x {p.d - shared_L} layers x {sub} compressions per subtree "
-                               f"(executed; {shared_L} top layers come from {units} shared subtrees)",
+            "work_per_launch": f"{chunk} msgs x {p.d - rshared_L} layers x {sub} compressions per subtree "
+                               f"(executed; {rshared_L} top layers come from {units} shared subtrees)",
             "kernel_ms": round(tree_ms_avg, 3),
             "peak_basis": f"{info['sm_count']} SMs x {sm_max:.0f} MHz x 128 / 1384",
         },
+        "step_fracs": step_fracs,
         "kernel_ms_graph": {k: round(v, 3) for k, v in graph_ms.items()},
         "kernel_ms_serial": {k: round(v, 3) for k, v in kt[0].items()},
         "hbm_sig_writeout_gbs": round(count * p.sig_bytes / (statistics.mean(step_ms) / 1e3) / 1e9, 3),
@@ -380,9 +468,14 @@ def measure_set(eng, info, set_id: str, count: int, steps: int, warmup: int, ran
     }
 
 
-# per-GPU message counts of the secondary sets reported beside the headline
-# (BASELINE configs[2]: 192f at 16384 messages; configs[3]/[4] 256f batches)
-OTHER_SETS = {"128f": 4096, "192f": 16384, "256f": 16384}
+# per-GPU message counts of the sets reported beside the headline (BASELINE
+# configs[1..3]: 128f at 4096, 192f at 16384, 256f at 65536 messages)
+OTHER_SETS = {"128f": 4096, "192f": 16384, "256f": 65536}
+
+
+def engine_config(cfg: dict) -> dict:
+    return {k: v for k, v in cfg.items() if k.startswith("fors") or k in ("variant", "streams", "chunk",
+                                                                        "shared_layers", "tree_split")}
 
 
 def run_ours(args):
@@ -395,7 +488,7 @@ def run_ours(args):
     info = eng.device_info()
     count = args.count
     r = measure_set(eng, info, args.set_id, count, args.steps, args.warmup, rank, world, dist, args.check)
-    p = r["p"]
+    cpu_ok = rank == 0 and world == 1 and not args.no_cpu_baseline
 
     others = {}
     if not args.single_set:
@@ -406,25 +499,21 @@ def run_ours(args):
                             small_batches=(1,))
             others[sid] = {
                 "value": round(o["value"], 1), "unit": "sig/s", "messages_per_gpu": n,
+                "config": bench_config(sid, n, world), "engine_config": engine_config(o["cfg"]),
                 "ms_per_step": round(1e3 * o["dev_s"] / min(args.steps, 5), 4),
                 "value_no_subtree_sharing": round(o["value_plain"], 1) if o["value_plain"] else None,
                 "subtree_sharing_layers": o["shared_L"],
                 "e2e": o["e2e"], "launch_latency": o["launch_latency"],
-                "roofline": {k: o["roofline"][k] for k in ("achieved", "peak", "unit", "frac", "kernel_ms")},
+                "roofline": {k: o["roofline"][k] for k in ("achieved", "peak", "unit", "frac", "kernel_ms",
+                                                           "work_per_launch")},
+                "step_fracs": o["step_fracs"],
                 "clocks": {"sm_mhz": o["clk"]["sm_mhz"], "reasons": o["clk"]["reasons"]},
                 "parity_spot_check": o["parity_spot_check"],
+                "cpu_baseline": (cpu_baseline_line(sid, o["sk"], o["msgs"], args.cpu_seconds / 2)
+                                 if cpu_ok else None),
             }
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sys.path.insert(0, str(ROOT / "oracle"))
-        import oracle  # CPU baseline leg only
-
-        threads = os.cpu_count() or 1
-        rate, n, dt = cpu_sign_rate(args.set_id, r["sk"], r["msgs"], args.cpu_seconds, threads)
-        cpu = {"value": round(rate, 3), "unit": "sig/s", "cores": threads, "kind": "port",
-               "sample": f"{n} of the same {args.set_id} messages in {dt:.1f}s, C oracle (oracle/hs_oracle.c, "
-                         f"SHA-NI={oracle.shani_active()})"}
+    cpu = cpu_baseline_line(args.set_id, r["sk"], r["msgs"], args.cpu_seconds) if cpu_ok else None
 
     if rank == 0:
         clk = r["clk"]
@@ -442,14 +531,11 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "u32",
             "data": "synthetic",
-            "config": {
-                "workload": f"SPHINCS+-{args.set_id} batched sign, {count} x 32-byte msgs per GPU, 1 key "
-                            f"(BASELINE configs[1])",
-                "set": args.set_id, "messages_per_gpu": count, "global_batch": world * count,
-                "parallelism": f"message-shard x{world}", "l2": "flushed between steps (256 MiB rewrite)",
-                "fors_layout": {k: v for k, v in cfg.items() if k.startswith("fors")},
-                "variant": cfg["variant"],
-            },
+            "config": bench_config(args.set_id, count, world),
+            "timing": {"l2": "flushed between steps (256 MiB rewrite outside the events)",
+                       "value": "CUDA events per step on the launching stream, max over ranks",
+                       "e2e": "host wall clock around hs_sign_batch_ex from pinned buffers, max over ranks"},
+            "engine_config": engine_config(cfg),
             "e2e": r["e2e"],
             "gpu_launches": int(r["launches"]),
             "launch_latency": r["launch_latency"],
@@ -461,6 +547,7 @@ def run_ours(args):
                                 "note": "top hypertree layers address few subtrees per key; each distinct "
                                         "(key, layer, tree) subtree is computed once per batch (bytes unchanged)"},
             "roofline": r["roofline"],
+            "step_fracs": r["step_fracs"],
             "kernel_ms_graph": r["kernel_ms_graph"],
             "kernel_ms_serial": r["kernel_ms_serial"],
             "hbm_sig_writeout_gbs": r["hbm_sig_writeout_gbs"],
@@ -477,6 +564,23 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.gpus < 1:
+        sys.exit("bench.py: --gpus must be >= 1")
+    if "WORLD_SIZE" in os.environ:
+        _, world, _ = dist_env()
+        if world != args.gpus:
+            sys.exit(f"bench.py: launched with WORLD_SIZE={world} but --gpus {args.gpus}")
+        if args.plan:
+            print(json.dumps({"launcher": "external", "ranks": world}))
+            return
+    elif args.gpus > 1 and args.impl == "ours":
+        if args.plan:
+            print(json.dumps({"launcher": "bench.py", "ranks": rank_plan(args.gpus, 0)}))
+            return
+        sys.exit(spawn_ranks(args.gpus))
+    elif args.plan:
+        print(json.dumps({"launcher": "none", "ranks": 1}))
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -19,6 +19,8 @@
  *   hs_config_get/set TuningConfig per-set row  config.py:33-60 (fusion, relax,
  *                     backends row backends.py:201-257)
  *   hs_params         params.derive             params.py:97-149
+ *   hs_tune           tuner.tree_tune + profile_kernels / select_backends
+ *                     tuner.py:91-143, 184-274 (cli.py:119-148 `tune`)
  *   hs_stage/hs_run/hs_fetch
  *                     GraphSigner.prepare / run_fors|run_tree|run_wots
  *                     (batchgraph.py:288-353): the stage plugin, split so the
@@ -191,6 +193,23 @@ HS_API int hs_variants(int32_t *masks, int cap);
  * Returns the number of values written.  (No reference counterpart: the
  * reference's batchgraph.py:245-353 runs its DAG on host threads.) */
 HS_API int hs_launch_stats(hs_t *h, double *out, int cap, int reset);
+
+/* On-device Tree Tuning (reference tuner.py:91-143 Algorithm 1 and the
+ * profiling / backend selection of tuner.py:184-274, driven from cli.py:119-148
+ * `tune`), run on this handle's device over `count` synthetic 32-byte messages
+ * signed with key row 0 (a fixed synthetic key when none is uploaded):
+ *   1. every FORS layout (N_tree, F, Relax) Algorithm 1 admits at S_max = the
+ *      device's opt-in shared memory is timed (FORS_Sign, CUDA events), the
+ *      `top` fastest re-timed `reps` times, the best trimmed mean kept; then
+ *      every split between in-CTA levels and level grids (fors_cta_levels);
+ *   2. per kernel, every compiled SHA-256 path; a non-native path replaces
+ *      native only when > 2% faster (the reference's tie rule);
+ *   3. the sub-batch stream count T, timed end to end (hs_sign_batch_ex).
+ * The handle is left configured with the result; json receives a report
+ * (layouts, timings, final hs_set_config).  Returns 0, or the report's size
+ * + 1 when cap is too small (truncated; the configuration is applied either
+ * way), or a negative HS_E_* code. */
+HS_API int hs_tune(hs_t *h, int set, uint32_t count, int32_t top, int32_t reps, char *json, size_t cap);
 
 /* Page-locked host memory for zero-copy-staging callers (cudaMallocHost). */
 HS_API void *hs_host_alloc(size_t bytes);

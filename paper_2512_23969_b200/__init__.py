@@ -5,7 +5,7 @@ byte-exact layouts) plus batch entry points; all hashing runs in the sm_100a
 kernels of libherosign_b200.so through its C-ABI.
 """
 
-from .engine import Engine, PinnedBuffer, get_engine
+from .engine import Engine, MultiEngine, PinnedBuffer, get_engine, get_multi_engine, shard_ranges
 from .errors import (ConfigError, FormatError, GraphExecutionError, HeroSignError, TuningError,
                      UsageError)
 from .params import PARAMETER_SETS, DerivedParams, ParameterSet, compressions_per_signature, derive
@@ -13,7 +13,7 @@ from .sigcore import (PublicKey, SecretKey, keygen, keygen_batch, message_to_ind
                       signature_regions, verify, verify_batch)
 
 __all__ = [
-    "Engine", "PinnedBuffer", "get_engine", "ConfigError", "FormatError", "GraphExecutionError",
+    "Engine", "MultiEngine", "PinnedBuffer", "get_engine", "get_multi_engine", "shard_ranges", "ConfigError", "FormatError", "GraphExecutionError",
     "HeroSignError", "TuningError", "UsageError", "PARAMETER_SETS", "DerivedParams", "ParameterSet",
     "compressions_per_signature", "derive", "PublicKey", "SecretKey", "keygen", "keygen_batch",
     "message_to_indices", "sign", "sign_batch", "signature_regions", "verify", "verify_batch",

@@ -29,7 +29,7 @@ HS_E_CUDA = -10
 EXPORTS = (
     "hs_open", "hs_close", "hs_last_error", "hs_device_info", "hs_params", "hs_config_get", "hs_config_set",
     "hs_fors_smem_bytes", "hs_keys_upload", "hs_keygen_batch", "hs_sign_batch", "hs_sign_batch_ex", "hs_verify_batch",
-    "hs_stage", "hs_run", "hs_sync", "hs_fetch", "hs_timings", "hs_bench_run", "hs_launch_count", "hs_launch_stats", "hs_variants", "hs_batch_info",
+    "hs_stage", "hs_run", "hs_sync", "hs_fetch", "hs_timings", "hs_bench_run", "hs_launch_count", "hs_launch_stats", "hs_variants", "hs_batch_info", "hs_tune",
     "hs_host_alloc", "hs_host_free",
 )
 
@@ -102,6 +102,7 @@ def lib() -> ctypes.CDLL:
         "hs_launch_stats": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.c_int]),
         "hs_variants": (ctypes.c_int, [ctypes.POINTER(i32), ctypes.c_int]),
         "hs_batch_info": (ctypes.c_int, [vp, ctypes.c_int, ctypes.POINTER(i32), ctypes.c_int]),
+        "hs_tune": (ctypes.c_int, [vp, ctypes.c_int, u32, i32, i32, ctypes.c_char_p, ctypes.c_size_t]),
         "hs_host_alloc": (vp, [ctypes.c_size_t]),
         "hs_host_free": (None, [vp]),
     }

@@ -310,23 +310,26 @@ int check_layout(hs_t* h, int set, const hs_set_config& c) {
   return HS_OK;
 }
 
+// Messages one graph launch signs: a staged batch larger than cfg.chunk runs
+// as consecutive launches of `chunk` messages over resident inputs, so the
+// per-message work buffers (stash, chain ends, FORS levels, ...) are sized for
+// one chunk and only the inputs and signatures for the whole batch.
+uint32_t work_count(const hs_set_config& c, uint32_t count) {
+  return std::min(count, (uint32_t)std::max(1, c.chunk));
+}
+
 int ensure_capacity(hs_t* h, int set, int slot, uint32_t count, size_t msg_bytes) {
   const SetInfo& I = kInfo[set];
   Buffers& B = h->buf[set];
   Slot& S = B.io[slot];
-  void* before[11] = {S.msgs, S.offs, S.keyidx, S.optrand, S.sigs, S.wsteps, B.plans, B.idx, B.roots, B.froots, B.stash};
+  void* before[6] = {S.msgs, S.offs, S.keyidx, S.optrand, S.sigs, S.wsteps};
   CUDA_TRY(h, grow(S.msgs, S.msgs_cap, std::max(msg_bytes, (size_t)1)));
   CUDA_TRY(h, grow(S.offs, S.offs_cap, (size_t)count + 1));
   CUDA_TRY(h, grow(S.keyidx, S.keyidx_cap, (size_t)count));
   CUDA_TRY(h, grow(S.optrand, S.optrand_cap, (size_t)count * I.n));
   CUDA_TRY(h, grow(S.sigs, S.sigs_cap, (size_t)count * I.sig_bytes));
   CUDA_TRY(h, grow(S.wsteps, S.wsteps_cap, (size_t)count));
-  CUDA_TRY(h, grow(B.plans, B.plans_cap, (size_t)count));
-  CUDA_TRY(h, grow(B.idx, B.idx_cap, (size_t)count * I.k));
-  CUDA_TRY(h, grow(B.roots, B.roots_cap, (size_t)count * (I.d + 1) * 8));
-  CUDA_TRY(h, grow(B.froots, B.froots_cap, (size_t)count * I.k * 8));
-  if (h->sets[set].cfg.wots_from_tree) CUDA_TRY(h, grow(B.stash, B.stash_cap, (size_t)count * stash_words(set)));
-  void* after[11] = {S.msgs, S.offs, S.keyidx, S.optrand, S.sigs, S.wsteps, B.plans, B.idx, B.roots, B.froots, B.stash};
+  void* after[6] = {S.msgs, S.offs, S.keyidx, S.optrand, S.sigs, S.wsteps};
   if (std::memcmp(before, after, sizeof before) != 0) {
     B.gen++;
     drop_graphs(h);
@@ -362,10 +365,12 @@ size_t chain_end_words(int set, uint32_t count) {
   return (size_t)count * I.d * I.leaves * I.wots_len * (I.n / 4);
 }
 
-// Arguments for messages [first, first + count) of the staged batch.  Message
-// offsets stay absolute into the staged blob; every per-message buffer is
-// offset by `first`, so sub-batches are independent launches.
-LaunchArgs make_args(hs_t* h, int set, uint32_t first, uint32_t count) {
+// Arguments for messages [io_first, io_first + count) of the staged batch,
+// whose per-message work buffers start at work_first (the message's index in
+// its chunk).  Message offsets stay absolute into the staged blob; every
+// per-message buffer is offset, so sub-batches are independent launches.
+LaunchArgs make_args(hs_t* h, int set, uint32_t io_first, uint32_t work_first, uint32_t count) {
+  const uint32_t first = work_first;
   const SetInfo& I = kInfo[set];
   SetState& St = h->sets[set];
   Buffers& B = h->buf[set];
@@ -375,12 +380,12 @@ LaunchArgs make_args(hs_t* h, int set, uint32_t first, uint32_t count) {
   a.keys = St.keys;
   a.nkeys = St.nkeys;
   a.msgs = S.msgs;
-  a.offs = S.offs + first;
-  a.key_idx = St.has_keyidx ? S.keyidx + first : nullptr;
-  a.opt_rand = St.has_optrand ? S.optrand + (size_t)first * I.n : nullptr;
+  a.offs = S.offs + io_first;
+  a.key_idx = St.has_keyidx ? S.keyidx + io_first : nullptr;
+  a.opt_rand = St.has_optrand ? S.optrand + (size_t)io_first * I.n : nullptr;
   a.count = count;
-  a.sigs = S.sigs + (size_t)first * I.sig_bytes;
-  a.wots_steps = S.wsteps ? S.wsteps + first : nullptr;
+  a.sigs = S.sigs + (size_t)io_first * I.sig_bytes;
+  a.wots_steps = S.wsteps ? S.wsteps + io_first : nullptr;
   a.plans = B.plans + first;
   a.indices = B.idx + (size_t)first * I.k;
   a.roots = B.roots + (size_t)first * (I.d + 1) * 8;
@@ -452,18 +457,25 @@ cudaError_t enqueue_fors(int set, const hs_set_config& c, const LaunchArgs& a, c
   return e;
 }
 
-// Config-dependent scratch for `count` messages: upper FORS levels and the
-// split TREE_Sign's chain ends.
+// Per-message work buffers for one launch of `count` messages: message plans,
+// FORS indices, roots, the WOTS stash, upper FORS levels and the split
+// TREE_Sign's chain ends.
 int ensure_scratch(hs_t* h, int set, uint32_t count) {
+  const SetInfo& I = kInfo[set];
   Buffers& B = h->buf[set];
   const hs_set_config& c = h->sets[set].cfg;
-  void* before[4] = {B.fnodes[0], B.fnodes[1], B.ends, B.lpre};
+  void* before[9] = {B.fnodes[0], B.fnodes[1], B.ends, B.lpre, B.plans, B.idx, B.roots, B.froots, B.stash};
+  CUDA_TRY(h, grow(B.plans, B.plans_cap, (size_t)count));
+  CUDA_TRY(h, grow(B.idx, B.idx_cap, (size_t)count * I.k));
+  CUDA_TRY(h, grow(B.roots, B.roots_cap, (size_t)count * (I.d + 1) * 8));
+  CUDA_TRY(h, grow(B.froots, B.froots_cap, (size_t)count * I.k * 8));
+  if (c.wots_from_tree) CUDA_TRY(h, grow(B.stash, B.stash_cap, (size_t)count * stash_words(set)));
   if (fors_node_words(set, c, count, 0) != 0) {
     for (int b = 0; b < 2; b++) CUDA_TRY(h, grow(B.fnodes[b], B.fnodes_cap[b], fors_node_words(set, c, count, b)));
     CUDA_TRY(h, grow(B.lpre, B.lpre_cap, (size_t)count * (kInfo[set].log_t + 1) * 8));
   }
   if (c.tree_split) CUDA_TRY(h, grow(B.ends, B.ends_cap, chain_end_words(set, count)));
-  void* after[4] = {B.fnodes[0], B.fnodes[1], B.ends, B.lpre};
+  void* after[9] = {B.fnodes[0], B.fnodes[1], B.ends, B.lpre, B.plans, B.idx, B.roots, B.froots, B.stash};
   if (std::memcmp(before, after, sizeof before) != 0) {
     B.gen++;
     drop_graphs(h);
@@ -557,9 +569,9 @@ void sub_range(uint32_t count, int T, int j, uint32_t& first, uint32_t& cn) {
 // sub-batch's signatures are complete (event done_j) while the others still
 // run, so their D2H copies (issued on ls[j] outside the graph) overlap the
 // remaining compute.  The shared-subtree kernel runs once for the whole batch.
-cudaError_t enqueue_batch(hs_t* h, int set, uint32_t count, int T, bool capture) {
+cudaError_t enqueue_batch(hs_t* h, int set, uint32_t io_first, uint32_t count, int T, bool capture) {
   const hs_set_config& c = h->sets[set].cfg;
-  const LaunchArgs all = make_args(h, set, 0, count);
+  const LaunchArgs all = make_args(h, set, io_first, 0, count);
   auto rec = [&](cudaEvent_t ev, cudaStream_t s) {
     return capture ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal) : cudaEventRecord(ev, s);
   };
@@ -583,7 +595,7 @@ cudaError_t enqueue_batch(hs_t* h, int set, uint32_t count, int T, bool capture)
     uint32_t first, cn;
     sub_range(count, T, j, first, cn);
     if (cn == 0) break;
-    const LaunchArgs a = make_args(h, set, first, cn);
+    const LaunchArgs a = make_args(h, set, io_first + first, first, cn);
     // TREE_j on priority 1+2j, FORS_j just below it: FORS_j's short CTAs fill
     // the SMs TREE_j drains before TREE_{j+1} claims them, and the last
     // sub-batch's FORS fills the final tail.
@@ -608,11 +620,55 @@ cudaError_t enqueue_batch(hs_t* h, int set, uint32_t count, int T, bool capture)
   return cudaSuccess;
 }
 
-// Sign the staged batch (io slot St.slot).  With fetch_to, sub-batch j's
-// signatures (and WOTS step counts, with wsteps_to) are copied to the host on
-// ls[j] as soon as that sub-batch completes; d2h_done[slot][j] marks the copy.
-// Nothing here waits for those copies: the next batch that reuses the slot
-// does (double-buffered chunks in hs_sign_batch).
+// One graph launch over messages [io_first, io_first + count) of the staged
+// batch (count <= cfg.chunk), T prioritised sub-batches.
+int launch_chunk(hs_t* h, int set, uint32_t io_first, uint32_t count, int T) {
+  SetState& St = h->sets[set];
+  if (!St.cfg.use_graph) {
+    CUDA_TRY(h, enqueue_batch(h, set, io_first, count, T, false));
+    return HS_OK;
+  }
+  GraphKey key{set, count, St.has_keyidx ? 1 : 0, St.has_optrand ? 1 : 0, h->buf[set].gen,
+               cfg_fingerprint(St.cfg) + "/" + std::to_string((uintptr_t)St.keys) + "/" + std::to_string(St.nkeys) +
+                   "/L" + std::to_string(St.shared_eff) + "/T" + std::to_string(T) + "/S" + std::to_string(St.slot) +
+                   "/F" + std::to_string(io_first)};
+  auto it = h->graphs.find(key);
+  if (it == h->graphs.end()) {
+    // bounded cache: a caller that keeps changing batch shapes or configs
+    // (the tuner, a service with many batch sizes) re-captures instead of
+    // accumulating executable graphs
+    if (h->graphs.size() >= kMaxGraphs) drop_graphs(h);
+    cudaGraph_t g;
+    CUDA_TRY(h, cudaStreamBeginCapture(h->s0, cudaStreamCaptureModeThreadLocal));
+    cudaError_t e = enqueue_batch(h, set, io_first, count, T, true);
+    cudaError_t e2 = cudaStreamEndCapture(h->s0, &g);
+    if (e != cudaSuccess) return fail(h, HS_E_CUDA, "capture: %s", cudaGetErrorString(e));
+    if (e2 != cudaSuccess) return fail(h, HS_E_CUDA, "end capture: %s", cudaGetErrorString(e2));
+    cudaGraphExec_t ex;
+    CUDA_TRY(h, cudaGraphInstantiateWithFlags(&ex, g, cudaGraphInstantiateFlagUseNodePriority));
+    cudaGraphDestroy(g);
+    h->launches -= h->last_kernels;  // capture does not launch
+    h->graph_kernels[key] = h->last_kernels;
+    it = h->graphs.emplace(key, ex).first;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  const cudaError_t le = cudaGraphLaunch(it->second, h->s0);
+  const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  CUDA_TRY(h, le);
+  h->glaunch_n++;
+  h->glaunch_us_sum += us;
+  h->glaunch_us_max = std::max(h->glaunch_us_max, us);
+  h->launches += h->graph_kernels[key];
+  return HS_OK;
+}
+
+// Sign the staged batch (io slot St.slot), as consecutive graph launches of
+// at most cfg.chunk messages over the resident inputs.  With fetch_to,
+// sub-batch j's signatures (and WOTS step counts, with wsteps_to) are copied
+// to the host on ls[j] as soon as that sub-batch completes;
+// d2h_done[slot][j] marks the copy.  Nothing here waits for those copies: the
+// next batch that reuses the slot does (double-buffered chunks in
+// hs_sign_batch_ex).  *T_out = the most sub-batch streams any launch used.
 int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nullptr, uint32_t* wsteps_to = nullptr,
               int* T_out = nullptr) {
   if (count == 0) return HS_OK;
@@ -622,72 +678,47 @@ int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nu
   const int slot = St.slot;
   Slot& S = h->buf[set].io[slot];
   const size_t sb = (size_t)kInfo[set].sig_bytes;
-  if (int rc = ensure_scratch(h, set, std::max(count, St.staged)); rc != HS_OK) return rc;
+  const uint32_t chunk = work_count(St.cfg, count);
+  if (int rc = ensure_scratch(h, set, chunk); rc != HS_OK) return rc;
   // inputs of this slot landed; earlier copies out of this slot's signatures finished
   CUDA_TRY(h, cudaStreamWaitEvent(h->s0, h->h2d_done[slot], 0));
   for (int j = 0; j < kMaxStreams; j++) CUDA_TRY(h, cudaStreamWaitEvent(h->s0, h->d2h_done[slot][j], 0));
-  if (mode == 1) {  // serialised kernels with per-kernel events (roofline timing)
-    CUDA_TRY(h, enqueue(h, set, make_args(h, set, 0, count), false, true));
+  if (mode == 1) {  // serialised kernels with per-kernel events (roofline timing): one chunk
+    if (count > chunk) return fail(h, HS_E_USAGE, "serialised timing runs at most one chunk (%u messages)", chunk);
+    CUDA_TRY(h, enqueue(h, set, make_args(h, set, 0, 0, count), false, true));
     CUDA_TRY(h, cudaEventRecord(h->compute_done[slot], h->s0));
     if (fetch_to) CUDA_TRY(h, cudaMemcpyAsync(fetch_to, S.sigs, count * sb, cudaMemcpyDeviceToHost, h->s0));
     if (wsteps_to) CUDA_TRY(h, cudaMemcpyAsync(wsteps_to, S.wsteps, count * 4, cudaMemcpyDeviceToHost, h->s0));
     if (T_out) *T_out = 0;
     return HS_OK;
   }
-  int T = std::max(1, std::min(St.cfg.streams, kMaxStreams));
-  T = (int)std::min<uint32_t>((uint32_t)T, std::max<uint32_t>(1u, count / 256u));
-  h->last_T = T;
-  if (St.cfg.use_graph) {
-    GraphKey key{set, count, St.has_keyidx ? 1 : 0, St.has_optrand ? 1 : 0, h->buf[set].gen,
-                 cfg_fingerprint(St.cfg) + "/" + std::to_string((uintptr_t)St.keys) + "/" + std::to_string(St.nkeys) +
-                     "/L" + std::to_string(St.shared_eff) + "/T" + std::to_string(T) + "/S" + std::to_string(slot)};
-    auto it = h->graphs.find(key);
-    if (it == h->graphs.end()) {
-      // bounded cache: a caller that keeps changing batch shapes or configs
-      // (the tuner, a service with many batch sizes) re-captures instead of
-      // accumulating executable graphs
-      if (h->graphs.size() >= kMaxGraphs) drop_graphs(h);
-      cudaGraph_t g;
-      CUDA_TRY(h, cudaStreamBeginCapture(h->s0, cudaStreamCaptureModeThreadLocal));
-      cudaError_t e = enqueue_batch(h, set, count, T, true);
-      cudaError_t e2 = cudaStreamEndCapture(h->s0, &g);
-      if (e != cudaSuccess) return fail(h, HS_E_CUDA, "capture: %s", cudaGetErrorString(e));
-      if (e2 != cudaSuccess) return fail(h, HS_E_CUDA, "end capture: %s", cudaGetErrorString(e2));
-      cudaGraphExec_t ex;
-      CUDA_TRY(h, cudaGraphInstantiateWithFlags(&ex, g, cudaGraphInstantiateFlagUseNodePriority));
-      cudaGraphDestroy(g);
-      h->launches -= h->last_kernels;  // capture does not launch
-      h->graph_kernels[key] = h->last_kernels;
-      it = h->graphs.emplace(key, ex).first;
+  int Tmax = 0;
+  for (uint32_t c0 = 0; c0 < count; c0 += chunk) {
+    const uint32_t cn = std::min(chunk, count - c0);
+    int T = std::max(1, std::min(St.cfg.streams, kMaxStreams));
+    T = (int)std::min<uint32_t>((uint32_t)T, std::max<uint32_t>(1u, cn / 256u));
+    h->last_T = T;
+    Tmax = std::max(Tmax, T);
+    if (int rc = launch_chunk(h, set, c0, cn, T); rc != HS_OK) return rc;
+    if (fetch_to || wsteps_to) {
+      for (int j = 0; j < T; j++) {
+        uint32_t first, n;
+        sub_range(cn, T, j, first, n);
+        if (n == 0) break;
+        first += c0;
+        CUDA_TRY(h, cudaStreamWaitEvent(h->ls[j], h->done[j], 0));
+        if (fetch_to)
+          CUDA_TRY(h, cudaMemcpyAsync(fetch_to + first * sb, S.sigs + first * sb, n * sb, cudaMemcpyDeviceToHost,
+                                      h->ls[j]));
+        if (wsteps_to)
+          CUDA_TRY(h, cudaMemcpyAsync(wsteps_to + first, S.wsteps + first, (size_t)n * 4, cudaMemcpyDeviceToHost,
+                                      h->ls[j]));
+        CUDA_TRY(h, cudaEventRecord(h->d2h_done[slot][j], h->ls[j]));
+      }
     }
-    const auto t0 = std::chrono::steady_clock::now();
-    const cudaError_t le = cudaGraphLaunch(it->second, h->s0);
-    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
-    CUDA_TRY(h, le);
-    h->glaunch_n++;
-    h->glaunch_us_sum += us;
-    h->glaunch_us_max = std::max(h->glaunch_us_max, us);
-    h->launches += h->graph_kernels[key];
-  } else {
-    CUDA_TRY(h, enqueue_batch(h, set, count, T, false));
   }
   CUDA_TRY(h, cudaEventRecord(h->compute_done[slot], h->s0));
-  if (fetch_to || wsteps_to) {
-    for (int j = 0; j < T; j++) {
-      uint32_t first, cn;
-      sub_range(count, T, j, first, cn);
-      if (cn == 0) break;
-      CUDA_TRY(h, cudaStreamWaitEvent(h->ls[j], h->done[j], 0));
-      if (fetch_to)
-        CUDA_TRY(h, cudaMemcpyAsync(fetch_to + first * sb, S.sigs + first * sb, cn * sb, cudaMemcpyDeviceToHost,
-                                    h->ls[j]));
-      if (wsteps_to)
-        CUDA_TRY(h, cudaMemcpyAsync(wsteps_to + first, S.wsteps + first, (size_t)cn * 4, cudaMemcpyDeviceToHost,
-                                    h->ls[j]));
-      CUDA_TRY(h, cudaEventRecord(h->d2h_done[slot][j], h->ls[j]));
-    }
-  }
-  if (T_out) *T_out = T;
+  if (T_out) *T_out = Tmax;
   return HS_OK;
 }
 
@@ -750,9 +781,12 @@ int stage_inputs(hs_t* h, int set, int slot, const uint8_t* msgs, const uint64_t
     }
     const int hp = kInfo[set].hp;
     int L = 0;
+    // messages per launch: a batch larger than the chunk builds the shared
+    // subtrees once per chunk
+    const size_t per_launch = work_count(St.cfg, count);
     while (L < St.cfg.shared_layers) {
       const size_t units_j = (size_t)1 << (hp * L);  // subtrees at depth L per key
-      if (St.cfg.shared_auto && units_j * used > 2 * (size_t)count) break;
+      if (St.cfg.shared_auto && units_j * std::min<size_t>(used, per_launch) > 2 * per_launch) break;
       if ((size_t)St.nkeys * shared_words(set, L + 1) * 4 > kSharedBudgetBytes) break;
       L++;
     }
@@ -1228,6 +1262,224 @@ int hs_launch_stats(hs_t* h, double* out, int cap, int reset) {
     h->glaunch_us_sum = h->glaunch_us_max = 0.0;
   }
   return n;
+}
+
+// ---------------------------------------------------------------------------
+// hs_tune: the on-device Tree Tuning search (reference tuner.py:91-143
+// Algorithm 1 + profile_kernels / select_backends tuner.py:184-274), run on
+// this handle's device.  Python's tuner.tune_on_device is the same search
+// driven from the host package; this entry point gives a C / FFI caller
+// the tuner without Python.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct TuneCand {
+  int nt, f, relax, lanes, passes;
+  size_t smem;
+  double sync, ut, us;
+};
+
+// Algorithm 1 over (N_tree, F, Relax) at S_max = the device's opt-in shared
+// memory and the FORS kernel's 768-lane CTA (tuner.device_candidates), no
+// alpha pruning, ordered by (sync, -U_T, -U_S, lanes, F).
+std::vector<TuneCand> tune_candidates(hs_t* h, int set) {
+  const SetInfo& I = kInfo[set];
+  std::vector<TuneCand> out;
+  for (int relax = 0; relax <= 1; relax++) {
+    const int lpt = relax ? I.t / 2 : I.t;
+    for (int nt = 1; nt * lpt <= kForsMaxLanes; nt++) {
+      const int sets_total = (I.k + nt - 1) / nt;
+      for (int f = 1; f <= std::max(1, I.k / nt); f++) {
+        const size_t smem = fors_smem(set, nt, f, relax);
+        if (smem > (size_t)h->smem_optin) break;
+        const int passes = (sets_total + f - 1) / f;
+        const double syncs = (double)(I.log_t - relax) * passes;
+        out.push_back(TuneCand{nt, f, relax, nt * lpt, passes, smem, syncs, (double)(nt * lpt) / kForsMaxLanes,
+                               (double)smem / h->smem_optin});
+      }
+    }
+  }
+  std::sort(out.begin(), out.end(), [](const TuneCand& a, const TuneCand& b) {
+    return std::make_tuple(a.sync, -a.ut, -a.us, a.lanes, a.f) < std::make_tuple(b.sync, -b.ut, -b.us, b.lanes, b.f);
+  });
+  return out;
+}
+
+double trimmed_mean(std::vector<float> v) {
+  std::sort(v.begin(), v.end());
+  if (v.size() >= 3) v = std::vector<float>(v.begin() + 1, v.end() - 1);
+  double acc = 0;
+  for (float x : v) acc += x;
+  return v.empty() ? 0.0 : acc / v.size();
+}
+
+// Device ms of one kernel stage (1 FORS_Sign + T_k, 2 TREE_Sign, 3 WOTS_Sign)
+// in `reps` serialised runs of the staged batch (CUDA events around it).
+int time_stage(hs_t* h, int set, uint32_t count, int stage, int reps, std::vector<float>& out) {
+  out.clear();
+  for (int r = 0; r < reps; r++) {
+    if (int rc = run_batch(h, set, count, 1); rc != HS_OK) return rc;
+    float ms[5];
+    if (hs_timings(h, ms, 5) != 5) return fail(h, HS_E_CUDA, "tune: timing events");
+    out.push_back(ms[1 + stage]);
+  }
+  return HS_OK;
+}
+
+std::string cfg_json(const hs_set_config& c) {
+  char b[512];
+  snprintf(b, sizeof b,
+           "{\"fors_trees_per_set\": %d, \"fors_sets_fused\": %d, \"fors_relax\": %d, \"variant\": [%d, %d, %d, %d], "
+           "\"use_graph\": %d, \"chunk\": %d, \"wots_from_tree\": %d, \"streams\": %d, \"shared_layers\": %d, "
+           "\"shared_auto\": %d, \"fors_cta_levels\": %d, \"tree_split\": %d}",
+           c.fors_trees_per_set, c.fors_sets_fused, c.fors_relax, c.variant[0], c.variant[1], c.variant[2],
+           c.variant[3], c.use_graph, c.chunk, c.wots_from_tree, c.streams, c.shared_layers, c.shared_auto,
+           c.fors_cta_levels, c.tree_split);
+  return b;
+}
+
+}  // namespace
+
+int hs_tune(hs_t* h, int set, uint32_t count, int32_t top, int32_t reps, char* json, size_t cap) {
+  if (!h || !valid_set(set) || count == 0 || top < 1 || reps < 1) return fail(h, HS_E_USAGE, "bad arguments");
+  CUDA_TRY(h, cudaSetDevice(h->device));
+  const SetInfo& I = kInfo[set];
+  SetState& St = h->sets[set];
+  // synthetic batch: the key table as uploaded (a fixed synthetic key when
+  // none is), count 32-byte messages from a fixed splitmix64 stream
+  if (St.nkeys == 0) {
+    std::vector<uint8_t> seed(3 * I.n), sk(4 * I.n);
+    for (int i = 0; i < 3 * I.n; i++) seed[i] = (uint8_t)i;
+    if (int rc = hs_keygen_batch(h, set, seed.data(), 1, sk.data()); rc != HS_OK) return rc;
+    if (int rc = hs_keys_upload(h, set, sk.data(), 1); rc != HS_OK) return rc;
+  }
+  std::vector<uint8_t> msgs((size_t)count * 32);
+  uint64_t x = 0x2512239690ull;
+  for (size_t i = 0; i < msgs.size(); i += 8) {
+    x += 0x9e3779b97f4a7c15ull;
+    uint64_t z = x;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    std::memcpy(&msgs[i], &z, 8);
+  }
+  std::vector<uint64_t> offs(count + 1);
+  for (uint32_t i = 0; i <= count; i++) offs[i] = 32ull * i;
+  const hs_set_config base = St.cfg;
+  hs_set_config c = base;
+  c.chunk = std::max<int>(c.chunk, (int)count);  // one launch per timed batch
+  if (int rc = hs_config_set(h, set, &c); rc != HS_OK) return rc;
+  if (int rc = stage_inputs(h, set, 0, msgs.data(), offs.data(), nullptr, nullptr, 0, count, false); rc != HS_OK)
+    return rc;
+  std::string js = "{\"set\": " + std::to_string(set) + ", \"count\": " + std::to_string(count) +
+                   ", \"smem_optin\": " + std::to_string(h->smem_optin);
+  std::vector<float> t;
+  // 1. every feasible layout once (2 runs, min), the `top` fastest re-timed
+  const std::vector<TuneCand> cands = tune_candidates(h, set);
+  if (cands.empty()) return fail(h, HS_E_CONFIG, "no feasible FORS layout under %d bytes", h->smem_optin);
+  std::vector<std::pair<double, size_t>> first;
+  for (size_t i = 0; i < cands.size(); i++) {
+    c.fors_trees_per_set = cands[i].nt;
+    c.fors_sets_fused = cands[i].f;
+    c.fors_relax = cands[i].relax;
+    if (int rc = hs_config_set(h, set, &c); rc != HS_OK) return rc;
+    if (int rc = time_stage(h, set, count, 1, 2, t); rc != HS_OK) return rc;
+    first.emplace_back(*std::min_element(t.begin(), t.end()), i);
+  }
+  std::sort(first.begin(), first.end());
+  js += ", \"candidates\": " + std::to_string(cands.size()) + ", \"layouts\": [";
+  double best_ms = 1e30;
+  size_t best = first[0].second;
+  for (int k = 0; k < top && k < (int)first.size(); k++) {
+    const TuneCand& cd = cands[first[k].second];
+    c.fors_trees_per_set = cd.nt;
+    c.fors_sets_fused = cd.f;
+    c.fors_relax = cd.relax;
+    if (int rc = hs_config_set(h, set, &c); rc != HS_OK) return rc;
+    if (int rc = time_stage(h, set, count, 1, reps, t); rc != HS_OK) return rc;
+    const double ms = trimmed_mean(t);
+    char b[256];
+    snprintf(b, sizeof b, "%s{\"trees_per_set\": %d, \"sets_fused\": %d, \"relax\": %d, \"lanes\": %d, "
+             "\"smem_bytes\": %zu, \"passes\": %d, \"fors_ms\": %.4f}", k ? ", " : "", cd.nt, cd.f, cd.relax,
+             cd.lanes, cd.smem, cd.passes, ms);
+    js += b;
+    if (ms < best_ms) best_ms = ms, best = first[k].second;
+  }
+  js += "]";
+  c.fors_trees_per_set = cands[best].nt;
+  c.fors_sets_fused = cands[best].f;
+  c.fors_relax = cands[best].relax;
+  // 1b. in-CTA FORS levels vs the batch-wide level grids for that layout
+  js += ", \"cta_levels_ms\": {";
+  int best_lc = -1;
+  double best_lc_ms = 1e30;
+  for (int lc = -1; lc <= I.log_t; lc++) {
+    if (lc == 0 && c.fors_relax) continue;
+    c.fors_cta_levels = lc;
+    if (int rc = hs_config_set(h, set, &c); rc != HS_OK) return rc;
+    if (int rc = time_stage(h, set, count, 1, reps, t); rc != HS_OK) return rc;
+    const double ms = trimmed_mean(t);
+    js += (lc == -1 ? "\"" : ", \"") + std::to_string(lc) + "\": " + std::to_string(ms);
+    if (ms < best_lc_ms) best_lc_ms = ms, best_lc = lc;
+  }
+  js += "}";
+  c.fors_cta_levels = best_lc;
+  // 2. SHA-256 path per kernel: the fastest compiled path replaces native only
+  //    when faster by more than 2% (tuner.py:206-218)
+  js += ", \"variant_ms\": {";
+  const char* kname[3] = {"FORS_Sign", "TREE_Sign", "WOTS_Sign"};
+  for (int k = 0; k < 3; k++) {
+    std::vector<double> ms(hs::kVariants);
+    for (int v = 0; v < hs::kVariants; v++) {
+      c.variant[k] = v;
+      if (int rc = hs_config_set(h, set, &c); rc != HS_OK) return rc;
+      if (int rc = time_stage(h, set, count, 1 + k, reps, t); rc != HS_OK) return rc;
+      ms[v] = trimmed_mean(t);
+    }
+    int bv = (int)(std::min_element(ms.begin(), ms.end()) - ms.begin());
+    if (!(ms[bv] < ms[0] * 0.98)) bv = 0;
+    c.variant[k] = bv;
+    js += std::string(k ? ", " : "") + "\"" + kname[k] + "\": [";
+    for (int v = 0; v < hs::kVariants; v++) js += (v ? ", " : "") + std::to_string(ms[v]);
+    js += "]";
+  }
+  js += "}";
+  // 3. sub-batch streams T, timed end to end through hs_sign_batch_ex into a
+  //    pinned buffer (each sub-batch's copy-out overlaps the others' compute)
+  uint8_t* hout = nullptr;
+  CUDA_TRY(h, cudaMallocHost(&hout, (size_t)count * I.sig_bytes));
+  js += ", \"streams_ms\": {";
+  int best_T = 1;
+  double best_T_ms = 1e30;
+  const int Ts[6] = {1, 2, 3, 4, 6, 8};
+  int rc = HS_OK;
+  for (int i = 0; i < 6 && rc == HS_OK; i++) {
+    c.streams = Ts[i];
+    rc = hs_config_set(h, set, &c);
+    if (rc == HS_OK) rc = hs_sign_batch_ex(h, set, msgs.data(), offs.data(), nullptr, nullptr, count, hout, nullptr);
+    std::vector<float> w;
+    for (int r = 0; r < reps && rc == HS_OK; r++) {
+      const auto t0 = std::chrono::steady_clock::now();
+      rc = hs_sign_batch_ex(h, set, msgs.data(), offs.data(), nullptr, nullptr, count, hout, nullptr);
+      w.push_back((float)std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+    if (rc != HS_OK) break;
+    const double ms = trimmed_mean(w);
+    js += (i ? ", \"" : "\"") + std::to_string(Ts[i]) + "\": " + std::to_string(ms);
+    if (ms < best_T_ms) best_T_ms = ms, best_T = Ts[i];
+  }
+  cudaFreeHost(hout);
+  if (rc != HS_OK) return rc;
+  js += "}";
+  c.streams = best_T;
+  c.chunk = base.chunk;
+  if (int r2 = hs_config_set(h, set, &c); r2 != HS_OK) return r2;
+  js += ", \"config\": " + cfg_json(c) + "}";
+  if (json && cap) {
+    std::strncpy(json, js.c_str(), cap - 1);
+    json[cap - 1] = '\0';
+  }
+  return js.size() + 1 > cap ? (int)(js.size() + 1) : HS_OK;
 }
 
 void* hs_host_alloc(size_t bytes) {

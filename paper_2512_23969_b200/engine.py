@@ -208,11 +208,15 @@ class Engine:
                                                     or not wots_steps.flags.c_contiguous):
             raise UsageError(f"wots_steps must be a contiguous uint32 array of {count}")
         with self._lock:
-            self._check(
-                _lib.lib().hs_sign_batch_ex(self._h, p.index, _u8ptr(blob), _u8ptr(offs),
-                                            _u8ptr(key_idx) if key_idx is not None else None, _u8ptr(opt_rand),
-                                            count, _u8ptr(out), _u8ptr(wots_steps)),
-                "hs_sign_batch_ex")
+            self._sign_into_nolock(p, blob, offs, count, out, key_idx, opt_rand, wots_steps)
+
+    def _sign_into_nolock(self, p, blob, offs, count, out, key_idx, opt_rand, wots_steps) -> None:
+        # the C call (arguments already validated); the caller holds this handle's lock
+        self._check(
+            _lib.lib().hs_sign_batch_ex(self._h, p.index, _u8ptr(blob), _u8ptr(offs),
+                                        _u8ptr(key_idx) if key_idx is not None else None, _u8ptr(opt_rand),
+                                        count, _u8ptr(out), _u8ptr(wots_steps)),
+            "hs_sign_batch_ex")
 
     def sign_batch(self, set_id: str, msgs: Sequence[bytes], key_idx: Sequence[int] | None = None,
                    opt_rand: Sequence[bytes] | bytes | None = None, counts: bool = False):
@@ -272,11 +276,14 @@ class Engine:
         blob, offs = pack_messages(msgs)
         kidx = None if key_idx is None else np.ascontiguousarray(key_idx, dtype=np.uint32)
         with self._lock:
-            self._check(_lib.lib().hs_verify_batch(self._h, p.index, _u8ptr(bytes(pkb)), len(pkb) // p.pk_bytes,
-                                                   _u8ptr(blob), _u8ptr(offs), _u8ptr(kidx), _u8ptr(sigblob),
-                                                   count, _u8ptr(ok)),
-                        "hs_verify_batch")
+            self._verify_nolock(p, bytes(pkb), blob, offs, count, sigblob, kidx, ok)
         return [bool(o) and g for o, g in zip(ok.tolist(), good)]
+
+    def _verify_nolock(self, p, pkb: bytes, blob, offs, count, sigs, kidx, ok) -> None:
+        self._check(_lib.lib().hs_verify_batch(self._h, p.index, _u8ptr(pkb), len(pkb) // p.pk_bytes,
+                                               _u8ptr(blob), _u8ptr(offs), _u8ptr(kidx), _u8ptr(sigs), count,
+                                               _u8ptr(ok)),
+                    "hs_verify_batch")
 
     def verify_into(self, set_id: str, pks: bytes, blob, offs: np.ndarray, count: int, sigs,
                     key_idx: np.ndarray | None = None) -> np.ndarray:
@@ -337,6 +344,25 @@ class Engine:
                 "hs_bench_run")
         return [float(x) for x in ms]
 
+    def tune(self, set_id: str, count: int = 2048, top: int = 12, reps: int = 5) -> dict:
+        """The native on-device Tree Tuning search (hs_tune): FORS layout,
+        in-CTA levels, SHA-256 path per kernel and sub-batch streams, timed on
+        this device; leaves the engine configured and returns the report."""
+        import json
+
+        cap = 1 << 16
+        buf = ctypes.create_string_buffer(cap)
+        with self._lock:
+            rc = _lib.lib().hs_tune(self._h, SET_INDEX[set_id], int(count), int(top), int(reps), buf, cap)
+        if rc < 0:
+            self._check(rc, "hs_tune")
+        if rc > 0:
+            raise HeroSignError(f"hs_tune report needs {rc} bytes (config applied)")
+        rep = json.loads(buf.value.decode())
+        c = rep["config"]
+        c["variant"] = dict(zip(KERNELS, c["variant"]))
+        return rep
+
     @property
     def launch_count(self) -> int:
         return int(_lib.lib().hs_launch_count(self._h))
@@ -389,8 +415,197 @@ class PinnedBuffer:
             pass
 
 
+def _addr(buf) -> int:
+    """Address of a host buffer (bytes / bytearray / numpy array / raw pointer)."""
+    ptr = _u8ptr(buf)
+    return int(ptr.value or 0) if ptr is not None else 0
+
+
+def shard_ranges(count: int, parts: int) -> list[tuple[int, int]]:
+    """Contiguous, balanced message ranges [first, first + n), one per device
+    (messages are independent; no collective)."""
+    if parts < 1:
+        raise UsageError("at least one device is required")
+    base, extra = divmod(count, parts)
+    out, first = [], 0
+    for g in range(parts):
+        n = base + (1 if g < extra else 0)
+        out.append((first, n))
+        first += n
+    return out
+
+
+class _AllLocks:
+    """Re-entrant lock over several engines' handle locks (taken in a fixed
+    order), so a multi-call sequence owns every device's key table and config."""
+
+    def __init__(self, locks):
+        self._locks = list(locks)
+
+    def acquire(self):
+        for lk in self._locks:
+            lk.acquire()
+        return True
+
+    def release(self):
+        for lk in reversed(self._locks):
+            lk.release()
+
+    __enter__ = acquire
+
+    def __exit__(self, *exc):
+        self.release()
+
+
+class MultiEngine:
+    """Batched signing over several devices of one node.
+
+    One ``Engine`` per entry of ``devices`` (a device may repeat: two handles on
+    one device sign concurrently); a batch is split into contiguous balanced
+    shards, each signed by its engine on its own host thread (ctypes releases
+    the GIL around the C call) and copied by that engine straight into the
+    caller's output at offset ``first * sig_bytes`` -- pinned outputs take the
+    device's D2H directly.  No collective runs on the signing path; the only
+    partition is by message, as the reference's m x T split
+    (batchgraph.py:110-121) is.  Same calls as ``Engine`` for keys, config,
+    signing and verification, so sigcore can drive it (``devices=``)."""
+
+    def __init__(self, devices, engines: list | None = None):
+        self.devices = [int(d) for d in devices]
+        if not self.devices:
+            raise UsageError("at least one device is required")
+        if engines is None:
+            engines, seen = [], set()
+            for d in self.devices:
+                if d in seen:  # another handle on a device already in use
+                    e = Engine(d)
+                    apply_tuned_config(e)
+                else:
+                    e = get_engine(d)
+                    seen.add(d)
+                engines.append(e)
+        self.engines = list(engines)
+        uniq = list({id(e): e for e in self.engines}.values())
+        self.lock = _AllLocks(e.lock for e in uniq)
+
+    def __len__(self) -> int:
+        return len(self.engines)
+
+    def upload_keys(self, set_id: str, sks) -> int:
+        blob = bytes(sks if isinstance(sks, (bytes, bytearray)) else b"".join(sks))
+        with self.lock:
+            return [e.upload_keys(set_id, blob) for e in self.engines][0]
+
+    def config(self, set_id: str) -> dict:
+        return self.engines[0].config(set_id)
+
+    def set_config(self, set_id: str, **kw) -> dict:
+        with self.lock:
+            return [e.set_config(set_id, **kw) for e in self.engines][0]
+
+    @staticmethod
+    def _parallel(jobs) -> None:
+        errors: list = []
+
+        def run(fn):
+            try:
+                fn()
+            except Exception as exc:  # surfaced after join
+                errors.append(exc)
+
+        threads = [threading.Thread(target=run, args=(fn,)) for fn in jobs]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        if errors:
+            raise errors[0]
+
+    def sign_into(self, set_id: str, blob, offs, count: int, out, key_idx=None, opt_rand=None,
+                  wots_steps=None) -> None:
+        """Engine.sign_into over all devices: shard g signs messages
+        [first, first + n) into ``out`` at ``first * sig_bytes``."""
+        p = derive(set_id)
+        offs = _offsets(offs, count)
+        key_idx = _key_index(key_idx, count)
+        if opt_rand is not None and not isinstance(opt_rand, int) and len(opt_rand) < count * p.n:
+            raise UsageError(f"opt_rand must be {p.n} bytes per message")
+        if isinstance(wots_steps, np.ndarray) and (wots_steps.dtype != np.uint32 or wots_steps.size < count
+                                                    or not wots_steps.flags.c_contiguous):
+            raise UsageError(f"wots_steps must be a contiguous uint32 array of {count}")
+        b_addr, o_addr = _addr(blob), _addr(out)
+        r_addr = _addr(opt_rand) if opt_rand is not None else 0
+        w_addr = _addr(wots_steps) if wots_steps is not None else 0
+        jobs = []
+        for eng, (first, n) in zip(self.engines, shard_ranges(count, len(self.engines))):
+            if n == 0:
+                continue
+            o = np.ascontiguousarray(offs[first:first + n + 1])
+            k = np.ascontiguousarray(key_idx[first:first + n]) if key_idx is not None else None
+            jobs.append(lambda eng=eng, first=first, n=n, o=o, k=k: eng._sign_into_nolock(
+                p, b_addr, o, n, o_addr + first * p.sig_bytes, k, r_addr + first * p.n if r_addr else None,
+                w_addr + 4 * first if w_addr else None))
+        with self.lock:  # the worker threads run under the caller's ownership of every handle
+            self._parallel(jobs)
+
+    def sign_batch(self, set_id: str, msgs, key_idx=None, opt_rand=None, counts: bool = False):
+        """Engine.sign_batch over all devices (same arguments and result)."""
+        p = derive(set_id)
+        count = len(msgs)
+        if not count:
+            return ([], []) if counts else []
+        blob, offs = pack_messages([bytes(m) for m in msgs])
+        kidx = _key_index(key_idx, count)
+        orand = None
+        if opt_rand is not None:
+            if isinstance(opt_rand, (bytes, bytearray)):
+                orand = bytes(opt_rand)
+            else:
+                if any(o is None for o in opt_rand):
+                    raise UsageError("resolve default opt_rand entries (PK.seed) before a multi-device sign")
+                orand = b"".join(opt_rand)
+            if len(orand) != count * p.n:
+                raise UsageError(f"opt_rand must be {p.n} bytes per message")
+        out = bytearray(count * p.sig_bytes)
+        steps = np.zeros(count, dtype=np.uint32)
+        self.sign_into(set_id, blob, offs, count, out, kidx, orand, steps)
+        sb = p.sig_bytes
+        sigs = [bytes(out[i * sb:(i + 1) * sb]) for i in range(count)]
+        return (sigs, [int(x) for x in steps]) if counts else sigs
+
+    def verify_batch(self, set_id: str, pks, msgs, sigs, key_idx=None) -> list[bool]:
+        """Engine.verify_batch over all devices."""
+        p = derive(set_id)
+        count = len(msgs)
+        if len(sigs) != count:
+            raise UsageError("one signature per message required")
+        if not count:
+            return []
+        pkb = bytes(pks if isinstance(pks, (bytes, bytearray)) else b"".join(pks))
+        if not pkb or len(pkb) % p.pk_bytes:
+            raise UsageError(f"public keys must be a multiple of {p.pk_bytes} bytes")
+        good = [len(x) == p.sig_bytes for x in sigs]
+        sigblob = b"".join(x if g else bytes(p.sig_bytes) for x, g in zip(sigs, good))
+        blob, offs = pack_messages([bytes(m) for m in msgs])
+        kidx = _key_index(key_idx, count)
+        ok = np.zeros(count, dtype=np.uint8)
+        b_addr, s_addr, ok_addr = _addr(blob), _addr(sigblob), _addr(ok)
+        jobs = []
+        for eng, (first, n) in zip(self.engines, shard_ranges(count, len(self.engines))):
+            if n == 0:
+                continue
+            o = np.ascontiguousarray(offs[first:first + n + 1])
+            k = np.ascontiguousarray(kidx[first:first + n]) if kidx is not None else None
+            jobs.append(lambda eng=eng, first=first, n=n, o=o, k=k: eng._verify_nolock(
+                p, pkb, b_addr, o, n, s_addr + first * p.sig_bytes, k, ok_addr + first))
+        with self.lock:
+            self._parallel(jobs)
+        return [bool(x) and g for x, g in zip(ok.tolist(), good)]
+
+
 _ENGINES: dict[int, Engine] = {}
 _ENGINES_LOCK = threading.Lock()
+_MULTI: dict[tuple, MultiEngine] = {}
 
 
 TUNED_CONFIG = _lib.PKG_DIR / "b200_tuned.json"
@@ -421,3 +636,16 @@ def get_engine(device: int | None = None) -> Engine:
             apply_tuned_config(eng)
             _ENGINES[dev] = eng
         return eng
+
+
+def get_multi_engine(devices) -> MultiEngine:
+    """Process-wide MultiEngine for a device list (e.g. ``range(8)``), built on
+    the per-device engines of ``get_engine``."""
+    key = tuple(int(d) for d in devices)
+    with _ENGINES_LOCK:
+        m = _MULTI.get(key)
+    if m is None:
+        m = MultiEngine(key)
+        with _ENGINES_LOCK:
+            m = _MULTI.setdefault(key, m)
+    return m

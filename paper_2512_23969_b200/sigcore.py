@@ -18,7 +18,7 @@ import os
 from dataclasses import dataclass
 from typing import Sequence
 
-from .engine import get_engine
+from .engine import get_engine, get_multi_engine
 from .errors import FormatError, UsageError
 from .params import DerivedParams, compressions_per_signature, derive
 
@@ -164,11 +164,15 @@ def sign_batch(
     relax=None,
     selection=None,
     ctx_out: list | None = None,
+    devices: Sequence[int] | None = None,
 ) -> list[bytes]:
-    """Sign a batch in one graph launch.  ``sk`` is one SecretKey or a list
-    (then ``key_idx[i]`` picks message i's key; default key 0)."""
-    return sign_on_engine(get_engine(), msgs, sk, params, key_idx=key_idx, opt_rand=opt_rand, fusion=fusion,
-                          relax=relax, selection=selection, ctx_out=ctx_out)
+    """Sign a batch in one graph launch per device.  ``sk`` is one SecretKey or
+    a list (then ``key_idx[i]`` picks message i's key; default key 0).
+    ``devices`` (e.g. ``range(8)``) shards the batch by message over those
+    GPUs (engine.MultiEngine); default: this process's device."""
+    eng = get_engine() if devices is None else get_multi_engine(devices)
+    return sign_on_engine(eng, msgs, sk, params, key_idx=key_idx, opt_rand=opt_rand, fusion=fusion, relax=relax,
+                          selection=selection, ctx_out=ctx_out)
 
 
 def sign_on_engine(
@@ -232,10 +236,11 @@ def verify(msg: bytes, sig: bytes, pk: PublicKey, params: DerivedParams | str) -
 
 
 def verify_batch(msgs: Sequence[bytes], sigs: Sequence[bytes], pk, params, *,
-                 key_idx: Sequence[int] | None = None) -> list[bool]:
+                 key_idx: Sequence[int] | None = None, devices: Sequence[int] | None = None) -> list[bool]:
     p = derive(params)
     pks = [k.to_bytes() if hasattr(k, "to_bytes") else bytes(k) for k in (pk if isinstance(pk, (list, tuple)) else [pk])]
-    return get_engine().verify_batch(p.id, pks, [bytes(m) for m in msgs], [bytes(s) for s in sigs], key_idx=key_idx)
+    eng = get_engine() if devices is None else get_multi_engine(devices)
+    return eng.verify_batch(p.id, pks, [bytes(m) for m in msgs], [bytes(s) for s in sigs], key_idx=key_idx)
 
 
 def message_to_indices(mhash: bytes, p: DerivedParams) -> list[int]:

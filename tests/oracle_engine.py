@@ -62,3 +62,34 @@ class OracleEngine:
             return sigs
         steps = [oracle_wots_steps(self.oracle, set_id, keys[k], m, o) for m, k, o in zip(msgs, kk, orand)]
         return sigs, steps
+
+
+class OracleHandle(OracleEngine):
+    """Per-device handle stand-in for ``MultiEngine`` on CPU: implements the raw
+    pointer-level shard call (``_sign_into_nolock``) by reading the caller's
+    buffers at the given addresses and writing the oracle's signatures and WOTS
+    step counts back at the shard's offsets -- so the sharding and offset
+    arithmetic of MultiEngine runs unchanged."""
+
+    def __init__(self, oracle, device: int = 0):
+        super().__init__(oracle)
+        self.device = device
+        self.shards: list[tuple[int, int]] = []  # (messages, output address) per call
+
+    def _sign_into_nolock(self, p, blob, offs, count, out, key_idx, opt_rand, wots_steps):
+        import ctypes
+
+        import numpy as np
+
+        keys = self._keys[p.id]
+        base = int(blob)
+        msgs = [ctypes.string_at(base + int(offs[i]), int(offs[i + 1] - offs[i])) for i in range(count)]
+        kk = [int(x) for x in key_idx] if key_idx is not None else [0] * count
+        self.shards.append((count, int(out)))
+        for i, (m, k) in enumerate(zip(msgs, kk)):
+            o = ctypes.string_at(int(opt_rand) + i * p.n, p.n) if opt_rand else None
+            sig = self.oracle.sign(p.id, keys[k], m, o)
+            ctypes.memmove(int(out) + i * p.sig_bytes, sig, p.sig_bytes)
+            if wots_steps:
+                v = np.array([oracle_wots_steps(self.oracle, p.id, keys[k], m, o)], dtype=np.uint32)
+                ctypes.memmove(int(wots_steps) + 4 * i, v.ctypes.data, 4)
