@@ -753,6 +753,19 @@ __global__ void __launch_bounds__(kTreeBlock) shared_root_kernel(LaunchArgs a) {
 // ---------------------------------------------------------------------------
 // 768 lanes keep the register budget at 85 per thread (65536 / 768).
 constexpr int kForsMaxLanes = 768;
+// per-set launch bound of fors_sign_kernel (<= kForsMaxLanes): a smaller bound
+// gives ptxas more registers per lane for layouts that use fewer lanes
+#ifndef HS_FORS_LB_S0
+#define HS_FORS_LB_S0 768
+#endif
+#ifndef HS_FORS_LB_S1
+#define HS_FORS_LB_S1 768
+#endif
+#ifndef HS_FORS_LB_S2
+#define HS_FORS_LB_S2 768
+#endif
+template <int S>
+constexpr int kForsLaunchBound = S == 0 ? HS_FORS_LB_S0 : S == 1 ? HS_FORS_LB_S1 : HS_FORS_LB_S2;
 // per-message PRF / F prefix states (16 words) and per-level H prefix states
 // ((log_t + 1) x 8 words, log_t <= 9) at the head of FORS_Sign's smem
 constexpr int kForsPrefixWords = 16 + 8 * 10;
@@ -816,7 +829,7 @@ __device__ __forceinline__ void fors_leaf(const uint32_t mid[8], const uint32_t*
 }
 
 template <int S, class V>
-__global__ void __launch_bounds__(kForsMaxLanes) fors_sign_kernel(LaunchArgs a) {
+__global__ void __launch_bounds__(kForsLaunchBound<S>) fors_sign_kernel(LaunchArgs a) {
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
   constexpr int t = Pr::t;

@@ -66,7 +66,22 @@ static __constant__ uint32_t c_pow2[33] = {
     1u << 18, 1u << 19, 1u << 20, 1u << 21, 1u << 22, 1u << 23, 1u << 24, 1u << 25, 1u << 26,
     1u << 27, 1u << 28, 1u << 29, 1u << 30, 1u << 31, 0u};
 
-__device__ __forceinline__ uint32_t rotr(uint32_t x, int r) { return __funnelshift_r(x, x, r); }
+// Rotations as plain shifts: LLVM turns them into a funnel-shift intrinsic
+// (SHF.R.W, one ALU instruction, the same as __funnelshift_r) that it can
+// constant-fold and hoist out of loops.  __funnelshift_r is inline PTX, which
+// NVVM treats as opaque: in the WOTS chain loop the rotations of the
+// chain-invariant schedule words (ADRS words, constant padding) were then
+// recomputed at every step.  HS_ROTR_ASM=1 restores the inline-PTX form.
+#ifndef HS_ROTR_ASM
+#define HS_ROTR_ASM 0
+#endif
+__device__ __forceinline__ uint32_t rotr(uint32_t x, int r) {
+#if HS_ROTR_ASM
+  return __funnelshift_r(x, x, r);
+#else
+  return (x >> r) | (x << ((32 - r) & 31));
+#endif
+}
 __device__ __forceinline__ uint32_t fma_add(uint32_t a, uint32_t b) { return a * c_one + b; }
 __device__ __forceinline__ uint32_t fma_shr(uint32_t x, int r) { return __umulhi(x, c_pow2[32 - r]); }
 __device__ __forceinline__ uint32_t fma_rotr(uint32_t x, int r) {
