@@ -118,24 +118,6 @@ def test_subtree_work_matches_reference_counter(golden, set_id):
     assert shared_units(set_id, 2) == 1 + p.subtree_leaves
 
 
-def test_cli_usage_errors(tmp_path):
-    from paper_2512_23969_b200 import cli
-
-    assert cli.main(["keygen", "128f", "--sk", str(tmp_path / "sk"), "--pk", str(tmp_path / "pk"),
-                     "--seed", "zz"]) == cli.EXIT_USAGE
-    assert cli.main(["keygen", "128f", "--sk", str(tmp_path / "sk"), "--pk", str(tmp_path / "pk"),
-                     "--seed", "00" * 47]) == cli.EXIT_USAGE
-    (tmp_path / "k").write_bytes(bytes(10))
-    (tmp_path / "m").write_bytes(b"x")
-    assert cli.main(["sign", "128f", "--key", str(tmp_path / "k"), "--message", str(tmp_path / "m"),
-                     "--out", str(tmp_path / "s")]) == cli.EXIT_USAGE
-    (tmp_path / "pk").write_bytes(bytes(32))
-    (tmp_path / "s").write_bytes(bytes(5))
-    assert cli.main(["verify", "128f", "--pk", str(tmp_path / "pk"), "--message", str(tmp_path / "m"),
-                     "--sig", str(tmp_path / "s")]) == cli.EXIT_VERIFY_FAIL
-    assert cli.main(["frobnicate"]) == 2
-
-
 def test_compiled_sha_paths(L):
     """hs_variants reports native, fast and the Mx<mask> paths listed in hs_variants.h."""
     names = _lib.variant_names()
