@@ -75,8 +75,15 @@ def run_set(eng, set_id: str, messages: int, nkeys: int, chunk: int, extra: int 
                 per_key_checked.add(int(kidx[i]))
             checked += len(todo)
     out.free()
+    # the same (last) chunk with inputs resident in HBM, device-timed: how much of
+    # the end-to-end rate the host path (staging, H2D, D2H) costs at this config
+    eng.stage(set_id, blob, offs, cn, key_idx=kidx)
+    eng.bench_run(set_id, cn, 1, 0, 0)
+    dev_ms = eng.bench_run(set_id, cn, 3, 0, 0)
+    dev_rate = cn / (sum(dev_ms) / len(dev_ms) / 1e3)
     return {"set": set_id, "messages": messages, "keys": nkeys, "sign_s": round(sign_s, 3),
-            "sig_per_s": round(messages / sign_s, 1), "keygen_s": round(keygen_s, 3),
+            "sig_per_s": round(messages / sign_s, 1), "device_sig_per_s": round(dev_rate, 1),
+            "e2e_over_device": round(messages / sign_s / dev_rate, 4), "keygen_s": round(keygen_s, 3),
             "keygen_per_s": round(nkeys / keygen_s, 1), "verify_per_s": round(verified / verify_s, 1),
             "verified": verified,
             "oracle_checked": checked, "keys_checked": len(per_key_checked)}
