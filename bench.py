@@ -140,6 +140,14 @@ def dist_env():
     return rank, world, local
 
 
+def rank_device(local: int) -> int:
+    """This rank's GPU: LOCAL_RANK.  HS_BENCH_ONE_DEVICE=1 puts every rank on
+    device 0 -- a check of the N-rank launch / barrier / max-over-ranks path on
+    a one-GPU box (the line then carries "ranks_share_device": true and its
+    numbers are not a scaling measurement)."""
+    return 0 if os.environ.get("HS_BENCH_ONE_DEVICE") == "1" else local
+
+
 def init_dist(world: int):
     if world <= 1:
         return None
@@ -486,7 +494,7 @@ def run_ours(args):
 
     import paper_2512_23969_b200 as hs
 
-    eng = hs.get_engine(local)
+    eng = hs.get_engine(rank_device(local))
     info = eng.device_info()
     count = args.count
     r = measure_set(eng, info, args.set_id, count, args.steps, args.warmup, rank, world, dist, args.check)
@@ -559,6 +567,8 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "other_sets": others or None,
         }
+        if world > 1 and rank_device(1) == 0:
+            line["ranks_share_device"] = True
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
