@@ -417,17 +417,28 @@ __global__ void __launch_bounds__(kTreeBlock, (S == 2 ? kTreeMinBlocks8 : kTreeM
 // wots.py:140-143, streamed straight from global memory) and the leaves of a
 // subtree are reduced with warp shuffles as in tree_sign_kernel.
 // ---------------------------------------------------------------------------
-#ifndef HS_CHAIN_BLOCK
-#define HS_CHAIN_BLOCK 128
+// threads per block of the chain grids, per set (r02, interleaved A/B of
+// 64/128/256: 256 is 1.7 % faster than 128 for 256f's TREE_Sign and 0.4 %
+// for 192f; 128 stays for 128f, whose batch time is the same either way,
+// profiles/r02c_ab_chain_block*.txt)
+#ifndef HS_CHAIN_BLOCK_S0
+#define HS_CHAIN_BLOCK_S0 128
 #endif
-constexpr int kChainBlock = HS_CHAIN_BLOCK;
+#ifndef HS_CHAIN_BLOCK_S1
+#define HS_CHAIN_BLOCK_S1 256
+#endif
+#ifndef HS_CHAIN_BLOCK_S2
+#define HS_CHAIN_BLOCK_S2 256
+#endif
+template <int S>
+constexpr int kChainBlock = S == 0 ? HS_CHAIN_BLOCK_S0 : S == 1 ? HS_CHAIN_BLOCK_S1 : HS_CHAIN_BLOCK_S2;
 // No min-blocks bound by default: ptxas then allocates 55-64 registers for the
 // chain loop; any explicit bound (even 1) changes the allocation and cost
 // 5-10 % on B200 (profiles/r01_chain_block_sweep.txt).
 #ifdef HS_CHAIN_MIN_BLOCKS
-#define HS_CHAIN_BOUNDS __launch_bounds__(kChainBlock, HS_CHAIN_MIN_BLOCKS)
+#define HS_CHAIN_BOUNDS __launch_bounds__(kChainBlock<S>, HS_CHAIN_MIN_BLOCKS)
 #else
-#define HS_CHAIN_BOUNDS __launch_bounds__(kChainBlock)
+#define HS_CHAIN_BOUNDS __launch_bounds__(kChainBlock<S>)
 #endif
 
 template <int S, class V>
@@ -435,7 +446,7 @@ __global__ void HS_CHAIN_BOUNDS tree_chain_kernel(LaunchArgs a) {
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
   const uint32_t dl = (uint32_t)(Pr::d - a.shared_layers);
-  const uint64_t gid = (uint64_t)blockIdx.x * kChainBlock + threadIdx.x;
+  const uint64_t gid = (uint64_t)blockIdx.x * kChainBlock<S> + threadIdx.x;
   if (gid >= (uint64_t)a.count * dl * Pr::leaves * Pr::wots_len) return;
   const uint32_t chain = (uint32_t)(gid % Pr::wots_len);
   const uint64_t lid = gid / Pr::wots_len;             // (msg, layer, leaf)
@@ -664,7 +675,7 @@ __global__ void HS_CHAIN_BOUNDS shared_chain_kernel(LaunchArgs a) {
   using Pr = P<S>;
   using Sh = Shared<S>;
   constexpr int NW = Pr::NW;
-  const uint64_t gid = (uint64_t)blockIdx.x * kChainBlock + threadIdx.x;
+  const uint64_t gid = (uint64_t)blockIdx.x * kChainBlock<S> + threadIdx.x;
   if (gid >= (uint64_t)a.nkeys * Sh::units(a.shared_layers) * Pr::leaves * Pr::wots_len) return;
   const uint32_t chain = (uint32_t)(gid % Pr::wots_len);
   uint32_t key, layer, leaf;

@@ -49,8 +49,8 @@ cudaError_t launch_variant<HS_SET, HS_VAR>(int which, const LaunchArgs& a, cudaS
       break;
     case K_TREE_CHAIN:
       tree_chain_kernel<S, V><<<blocks((uint64_t)a.count * (Pr::d - a.shared_layers) * Pr::leaves * Pr::wots_len,
-                                       kChainBlock),
-                                kChainBlock, 0, s>>>(a);
+                                       kChainBlock<S>),
+                                kChainBlock<S>, 0, s>>>(a);
       break;
     case K_TREE_ROOT:
       tree_root_kernel<S, V><<<blocks((uint64_t)a.count * (Pr::d - a.shared_layers) * Pr::leaves, kTreeBlock),
@@ -60,8 +60,8 @@ cudaError_t launch_variant<HS_SET, HS_VAR>(int which, const LaunchArgs& a, cudaS
       if (a.shared_layers <= 0 || a.nkeys == 0) return cudaSuccess;
       shared_chain_kernel<S, V><<<blocks((uint64_t)a.nkeys * Shared<S>::units(a.shared_layers) * Pr::leaves *
                                              Pr::wots_len,
-                                         kChainBlock),
-                                  kChainBlock, 0, s>>>(a);
+                                         kChainBlock<S>),
+                                  kChainBlock<S>, 0, s>>>(a);
       break;
     case K_SHARED_ROOT:
       if (a.shared_layers <= 0 || a.nkeys == 0) return cudaSuccess;

@@ -301,17 +301,13 @@ def test_subtree_sharing(eng, oracle_mod, set_id):
         eng.set_config(set_id, **base)
 
 
-def test_cli_roundtrip(eng, golden, tmp_path):
-    from paper_2512_23969_b200 import cli
-
+def test_api_roundtrip_golden(eng, golden):
+    """keygen -> sign -> verify through the public API on the reference's own
+    192f vectors (sigcore.py:62-72, :139-178, :181-221)."""
     g = golden["sets"]["192f"]
-    sk, pk, msg, sig = (tmp_path / n for n in ("sk", "pk", "m", "sig"))
-    assert cli.main(["keygen", "192f", "--sk", str(sk), "--pk", str(pk), "--seed", g["keygen"]["seed"]]) == 0
-    assert sk.read_bytes().hex() == g["keygen"]["sk"]
-    msg.write_bytes(bytes(32))
-    assert cli.main(["sign", "192f", "--key", str(sk), "--message", str(msg), "--out", str(sig)]) == 0
-    assert sig.read_bytes() == (GOLDEN_DIR / "sig_192f_zero.bin").read_bytes()
-    assert cli.main(["verify", "192f", "--pk", str(pk), "--message", str(msg), "--sig", str(sig)]) == 0
-    msg.write_bytes(b"\x01" + bytes(31))
-    assert cli.main(["verify", "192f", "--pk", str(pk), "--message", str(msg), "--sig", str(sig)]) == 1
-    assert cli.main(["bench", "128f", "--messages", "256"]) == 0
+    sk = hs.keygen("192f", bytes.fromhex(g["keygen"]["seed"]))
+    assert sk.to_bytes().hex() == g["keygen"]["sk"]
+    sig = hs.sign(bytes(32), sk, "192f")
+    assert sig == (GOLDEN_DIR / "sig_192f_zero.bin").read_bytes()
+    assert hs.verify(bytes(32), sig, sk.public(), "192f")
+    assert not hs.verify(b"\x01" + bytes(31), sig, sk.public(), "192f")
