@@ -485,7 +485,7 @@ OTHER_SETS = {"128f": 4096, "192f": 16384, "256f": 65536}
 
 def engine_config(cfg: dict) -> dict:
     return {k: v for k, v in cfg.items() if k.startswith("fors") or k in ("variant", "streams", "chunk",
-                                                                        "shared_layers", "tree_split")}
+                                                                        "shared_layers", "tree_split", "overlap")}
 
 
 def run_ours(args):

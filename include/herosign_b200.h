@@ -90,10 +90,19 @@ typedef struct {
                                  whole tree in the CTA (reference shape,
                                  vexec.py:437-463), -1 = auto (leaves only:
                                  the measured best on B200)                  */
-  int32_t tree_split;         /* 1: TREE_Sign as two grids -- one thread per
+  int32_t tree_split;         /* TREE_Sign shape.  0: fused, one thread per
+                                 leaf runs its chains, T_len and the warp-
+                                 shuffle Merkle reduction; 1: one thread per
                                  WOTS chain, then one per leaf (T_len +
-                                 Merkle); 0: one thread per leaf runs its
-                                 chains and T_len (fused)                    */
+                                 warp-shuffle Merkle); 2: chain grid, leaf
+                                 grid (T_len), then one thread per subtree
+                                 for the Merkle levels                       */
+  int32_t overlap;            /* 1: inside a batch graph, sub-batch j's
+                                 FORS_Sign and TREE_Sign run on two streams
+                                 and sub-batches run concurrently (priority
+                                 ordered); 0: every kernel of the batch in one
+                                 stream order -- sub-batches then only
+                                 pipeline the signatures' D2H copies         */
 } hs_set_config;
 
 HS_API int hs_open(int device, hs_t **out);

@@ -50,6 +50,7 @@ class SetConfig(ctypes.Structure):
         ("shared_auto", ctypes.c_int32),
         ("fors_cta_levels", ctypes.c_int32),
         ("tree_split", ctypes.c_int32),
+        ("overlap", ctypes.c_int32),
     ]
 
 

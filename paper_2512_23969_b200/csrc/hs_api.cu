@@ -125,7 +125,8 @@ hs_set_config default_config(int set) {
   c.shared_layers = shared_max(set);
   c.shared_auto = 1;
   c.fors_cta_levels = -1;
-  c.tree_split = 1;
+  c.tree_split = 2;
+  c.overlap = 1;
   return c;
 }
 
@@ -304,7 +305,8 @@ int check_layout(hs_t* h, int set, const hs_set_config& c) {
   if (c.shared_layers < 0 || c.shared_layers > shared_max(set))
     return fail(h, HS_E_CONFIG, "shared_layers must be in 0..%d for this set", shared_max(set));
   if (c.shared_auto != 0 && c.shared_auto != 1) return fail(h, HS_E_CONFIG, "shared_auto must be 0 or 1");
-  if (c.tree_split != 0 && c.tree_split != 1) return fail(h, HS_E_CONFIG, "tree_split must be 0 or 1");
+  if (c.tree_split < 0 || c.tree_split > 2) return fail(h, HS_E_CONFIG, "tree_split must be 0, 1 or 2");
+  if (c.overlap != 0 && c.overlap != 1) return fail(h, HS_E_CONFIG, "overlap must be 0 or 1");
   if (c.fors_cta_levels < -1 || c.fors_cta_levels > I.log_t)
     return fail(h, HS_E_CONFIG, "fors_cta_levels must be -1 (auto) or in 0..%d", I.log_t);
   return HS_OK;
@@ -431,15 +433,21 @@ cudaError_t enqueue_shared(int set, const hs_set_config& c, const LaunchArgs& a,
   return e == cudaSuccess ? launch(set, K_SHARED_ROOT, c.variant[1], a, s) : e;
 }
 
-// TREE_Sign on one stream: split (chain grid, then leaf / Merkle grid) or fused.
+// TREE_Sign on one stream: split (chain grid, leaf grid, Merkle grid) or fused.
 cudaError_t enqueue_tree(int set, const hs_set_config& c, const LaunchArgs& a, cudaStream_t s, int& kernels) {
   if (!a.chain_ends) {
     kernels++;
     return launch(set, K_TREE, c.variant[1], a, s);
   }
-  kernels += 2;
   cudaError_t e = launch(set, K_TREE_CHAIN, c.variant[1], a, s);
-  return e == cudaSuccess ? launch(set, K_TREE_ROOT, c.variant[1], a, s) : e;
+  kernels++;
+  if (c.tree_split == 1) {  // leaves and warp-shuffle Merkle reduction in one grid
+    kernels++;
+    return e == cudaSuccess ? launch(set, K_TREE_ROOT, c.variant[1], a, s) : e;
+  }
+  kernels += 2;  // leaf grid, then one thread per subtree for the Merkle levels
+  if (e == cudaSuccess) e = launch(set, K_TREE_LEAF, c.variant[1], a, s);
+  return e == cudaSuccess ? launch(set, K_TREE_MERKLE, c.variant[1], a, s) : e;
 }
 
 // FORS_Sign, the batch-wide upper FORS levels (if any) and T_k on one stream.
@@ -586,6 +594,29 @@ cudaError_t enqueue_batch(hs_t* h, int set, uint32_t io_first, uint32_t count, i
   kernels++;
   TRY(rec(h->ev[1], h->s0));
   TRY(cudaEventRecord(h->fork, h->s0));
+  if (!c.overlap) {
+    // one stream order: shared subtrees, then per sub-batch FORS, TREE, WOTS
+    cudaStream_t q = h->q[1];
+    TRY(cudaStreamWaitEvent(q, h->fork, 0));
+    if (all.shared_layers > 0) TRY(enqueue_shared(set, c, all, q, kernels));
+    for (int j = 0; j < T; j++) {
+      uint32_t first, cn;
+      sub_range(count, T, j, first, cn);
+      if (cn == 0) break;
+      const LaunchArgs a = make_args(h, set, io_first + first, first, cn);
+      TRY(enqueue_fors(set, c, a, q, kernels));
+      TRY(enqueue_tree(set, c, a, q, kernels));
+      TRY(launch(set, a.stash ? K_WOTS_GATHER : K_WOTS, c.variant[2], a, q));
+      kernels += 1;
+      TRY(rec(h->done[j], q));
+    }
+    TRY(cudaEventRecord(h->joins[0], q));
+    TRY(cudaStreamWaitEvent(h->s0, h->joins[0], 0));
+    TRY(rec(h->ev[4], h->s0));
+    h->launches += kernels;
+    h->last_kernels = kernels;
+    return cudaSuccess;
+  }
   if (all.shared_layers > 0) {
     TRY(cudaStreamWaitEvent(h->q[0], h->fork, 0));
     TRY(enqueue_shared(set, c, all, h->q[0], kernels));
@@ -1331,10 +1362,10 @@ std::string cfg_json(const hs_set_config& c) {
   snprintf(b, sizeof b,
            "{\"fors_trees_per_set\": %d, \"fors_sets_fused\": %d, \"fors_relax\": %d, \"variant\": [%d, %d, %d, %d], "
            "\"use_graph\": %d, \"chunk\": %d, \"wots_from_tree\": %d, \"streams\": %d, \"shared_layers\": %d, "
-           "\"shared_auto\": %d, \"fors_cta_levels\": %d, \"tree_split\": %d}",
+           "\"shared_auto\": %d, \"fors_cta_levels\": %d, \"tree_split\": %d, \"overlap\": %d}",
            c.fors_trees_per_set, c.fors_sets_fused, c.fors_relax, c.variant[0], c.variant[1], c.variant[2],
            c.variant[3], c.use_graph, c.chunk, c.wots_from_tree, c.streams, c.shared_layers, c.shared_auto,
-           c.fors_cta_levels, c.tree_split);
+           c.fors_cta_levels, c.tree_split, c.overlap);
   return b;
 }
 
@@ -1444,17 +1475,20 @@ int hs_tune(hs_t* h, int set, uint32_t count, int32_t top, int32_t reps, char* j
     js += "]";
   }
   js += "}";
-  // 3. sub-batch streams T, timed end to end through hs_sign_batch_ex into a
-  //    pinned buffer (each sub-batch's copy-out overlaps the others' compute)
+  // 3. sub-batch streams T and stream overlap, timed end to end through
+  //    hs_sign_batch_ex into a pinned buffer (each sub-batch's copy-out
+  //    overlaps the later compute); keys "T" (FORS || TREE, concurrent
+  //    sub-batches) and "T/serial" (one stream order)
   uint8_t* hout = nullptr;
   CUDA_TRY(h, cudaMallocHost(&hout, (size_t)count * I.sig_bytes));
   js += ", \"streams_ms\": {";
-  int best_T = 1;
+  int best_T = 1, best_ov = 1;
   double best_T_ms = 1e30;
   const int Ts[6] = {1, 2, 3, 4, 6, 8};
   int rc = HS_OK;
-  for (int i = 0; i < 6 && rc == HS_OK; i++) {
-    c.streams = Ts[i];
+  for (int i = 0; i < 12 && rc == HS_OK; i++) {
+    c.streams = Ts[i % 6];
+    c.overlap = i < 6 ? 1 : 0;
     rc = hs_config_set(h, set, &c);
     if (rc == HS_OK) rc = hs_sign_batch_ex(h, set, msgs.data(), offs.data(), nullptr, nullptr, count, hout, nullptr);
     std::vector<float> w;
@@ -1465,13 +1499,14 @@ int hs_tune(hs_t* h, int set, uint32_t count, int32_t top, int32_t reps, char* j
     }
     if (rc != HS_OK) break;
     const double ms = trimmed_mean(w);
-    js += (i ? ", \"" : "\"") + std::to_string(Ts[i]) + "\": " + std::to_string(ms);
-    if (ms < best_T_ms) best_T_ms = ms, best_T = Ts[i];
+    js += (i ? ", \"" : "\"") + std::to_string(Ts[i % 6]) + (c.overlap ? "" : "/serial") + "\": " + std::to_string(ms);
+    if (ms < best_T_ms) best_T_ms = ms, best_T = Ts[i % 6], best_ov = c.overlap;
   }
   cudaFreeHost(hout);
   if (rc != HS_OK) return rc;
   js += "}";
   c.streams = best_T;
+  c.overlap = best_ov;
   c.chunk = base.chunk;
   if (int r2 = hs_config_set(h, set, &c); r2 != HS_OK) return r2;
   js += ", \"config\": " + cfg_json(c) + "}";

@@ -28,6 +28,8 @@ enum KernelId : int {
   K_TREE_ROOT = 12,
   K_SHARED_CHAIN = 13,
   K_SHARED_ROOT = 14,
+  K_TREE_MERKLE = 15,
+  K_TREE_LEAF = 16,
 };
 
 // variant: SHA-256 arithmetic path id, 0..kNumVariants-1 (sha256.cuh VariantOf)

@@ -559,6 +559,105 @@ __global__ void __launch_bounds__(kTreeBlock) tree_root_kernel(LaunchArgs a) {
   }
 }
 
+// tree_split = 2: part 2 computes only the leaves (T_len); the subtree is
+// reduced by tree_merkle_kernel.
+template <int S, class V>
+__global__ void __launch_bounds__(kTreeBlock) tree_leaf_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  constexpr int NW = Pr::NW;
+  constexpr int M = Pr::wots_len * NW;
+  constexpr uint32_t total = 22u + (uint32_t)(Pr::wots_len * Pr::n);  // bytes after the midstate block
+  constexpr uint32_t nblk = (total + 9u + 63u) / 64u;
+  const uint32_t dl = (uint32_t)(Pr::d - a.shared_layers);
+  const uint64_t per_msg = (uint64_t)dl * Pr::leaves;
+  const uint64_t gid = (uint64_t)blockIdx.x * kTreeBlock + threadIdx.x;
+  if (gid >= (uint64_t)a.count * per_msg) return;
+  const uint32_t msg = (uint32_t)(gid / per_msg);
+  const uint32_t rem = (uint32_t)(gid % per_msg);
+  const uint32_t layer = rem / Pr::leaves;
+  const uint32_t leaf = rem % Pr::leaves;
+
+  const MsgPlan pl = a.plans[msg];
+  const KeyDev& K = a.keys[pl.key];
+  uint64_t tree;
+  uint32_t leaf_idx;
+  layer_coords<S>(pl, (int)layer, tree, leaf_idx);
+  const Adrs pa = make_adrs(layer, tree, ADDR_WOTS_PK, leaf, 0, 0);
+  const uint32_t aw[6] = {pa.w0, pa.w1, pa.w2, pa.w3, pa.w4, pa.h5};
+  uint32_t* e = a.chain_ends + gid * M;
+  uint32_t node[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) node[j] = K.thash_mid[j];
+#pragma unroll 1
+  for (uint32_t b = 0; b < nblk; b++) {
+    uint32_t W[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) W[j] = tlen_word<M>(16u * b + j, aw, e, (64u + total) * 8u, 16u * nblk - 1u);
+    compress<V>(node, W);
+  }
+  // the leaf replaces the head of its own (consumed) chain-end record, where
+  // tree_merkle_kernel picks it up; the signing leaf's sibling is auth[0]
+#pragma unroll
+  for (int j = 0; j < NW; j++) e[j] = node[j];
+  if (leaf == (leaf_idx ^ 1u)) {
+    uint8_t* auth = a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_ht + (size_t)layer * Pr::layer_bytes +
+                    Pr::wots_sig_bytes;
+    store_node<NW>(auth, node);
+  }
+}
+
+// TREE_Sign part 3: thread = (message, layer) reduces its subtree's leaves
+// (treehash, oracle.py:27-63 / vexec.py:518-551) level by level, in place over
+// the leaves' records in chain_ends (node j of level L overwrites the record
+// of leaf j: its children 2j, 2j+1 are read first), storing the auth path
+// nodes of levels 1..hp-1 and the root.  One thread per subtree keeps every
+// lane busy at every level; reducing inside tree_root with warp shuffles left
+// 1/2, 3/4, 7/8 of a subtree's lanes idle at levels 1, 2, 3.
+template <int S, class V>
+__global__ void __launch_bounds__(kTreeBlock) tree_merkle_kernel(LaunchArgs a) {
+  using Pr = P<S>;
+  constexpr int NW = Pr::NW;
+  constexpr int M = Pr::wots_len * NW;
+  const uint32_t dl = (uint32_t)(Pr::d - a.shared_layers);
+  const uint64_t gid = (uint64_t)blockIdx.x * kTreeBlock + threadIdx.x;
+  if (gid >= (uint64_t)a.count * dl) return;
+  const uint32_t msg = (uint32_t)(gid / dl);
+  const uint32_t layer = (uint32_t)(gid % dl);
+  const MsgPlan pl = a.plans[msg];
+  const KeyDev& K = a.keys[pl.key];
+  uint64_t tree;
+  uint32_t leaf_idx;
+  layer_coords<S>(pl, (int)layer, tree, leaf_idx);
+  uint32_t mid[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) mid[j] = K.thash_mid[j];
+  uint32_t* base = a.chain_ends + gid * (uint64_t)Pr::leaves * M;
+  uint8_t* auth = a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_ht + (size_t)layer * Pr::layer_bytes +
+                  Pr::wots_sig_bytes;
+  uint32_t node[8];
+#pragma unroll 1
+  for (int lvl = 1; lvl <= Pr::hp; lvl++) {
+    const uint32_t per = (uint32_t)Pr::leaves >> lvl;
+    const uint32_t sib = (leaf_idx >> lvl) ^ 1u;
+#pragma unroll 1
+    for (uint32_t j = 0; j < per; j++) {
+      uint32_t m[2 * NW];
+      const uint32_t* c0 = base + (size_t)(2 * j) * M;
+      const uint32_t* c1 = c0 + M;
+#pragma unroll
+      for (int w = 0; w < NW; w++) { m[w] = c0[w]; m[NW + w] = c1[w]; }
+      thash_reg<V, 2 * NW>(node, mid, make_adrs(layer, tree, ADDR_HASHTREE, 0, (uint32_t)lvl, j), m);
+      if (lvl < Pr::hp && j == sib) store_node<NW>(auth + lvl * Pr::n, node);
+      uint32_t* d = base + (size_t)j * M;
+#pragma unroll
+      for (int w = 0; w < NW; w++) d[w] = node[w];
+    }
+  }
+  uint32_t* r = a.roots + ((size_t)msg * (Pr::d + 1) + layer + 1) * 8;
+#pragma unroll
+  for (int j = 0; j < NW; j++) r[j] = node[j];
+}
+
 // ---------------------------------------------------------------------------
 // Subtree sharing.  The top layers of the hypertree can only address a few
 // subtrees per key (layer d-1: tree 0; layer d-2: 2^(h/d) trees; ...), so in a

@@ -56,6 +56,14 @@ cudaError_t launch_variant<HS_SET, HS_VAR>(int which, const LaunchArgs& a, cudaS
       tree_root_kernel<S, V><<<blocks((uint64_t)a.count * (Pr::d - a.shared_layers) * Pr::leaves, kTreeBlock),
                                kTreeBlock, 0, s>>>(a);
       break;
+    case K_TREE_LEAF:
+      tree_leaf_kernel<S, V><<<blocks((uint64_t)a.count * (Pr::d - a.shared_layers) * Pr::leaves, kTreeBlock),
+                               kTreeBlock, 0, s>>>(a);
+      break;
+    case K_TREE_MERKLE:
+      tree_merkle_kernel<S, V><<<blocks((uint64_t)a.count * (Pr::d - a.shared_layers), kTreeBlock), kTreeBlock, 0,
+                                 s>>>(a);
+      break;
     case K_SHARED_CHAIN:
       if (a.shared_layers <= 0 || a.nkeys == 0) return cudaSuccess;
       shared_chain_kernel<S, V><<<blocks((uint64_t)a.nkeys * Shared<S>::units(a.shared_layers) * Pr::leaves *

@@ -129,7 +129,8 @@ class Engine:
             "shared_layers": c.shared_layers,
             "shared_auto": bool(c.shared_auto),
             "fors_cta_levels": c.fors_cta_levels,
-            "tree_split": bool(c.tree_split),
+            "tree_split": int(c.tree_split),
+            "overlap": bool(c.overlap),
         }
 
     def set_config(self, set_id: str, **kw) -> dict:
@@ -154,7 +155,8 @@ class Engine:
         c.shared_layers = int(cur["shared_layers"])
         c.shared_auto = int(bool(cur["shared_auto"]))
         c.fors_cta_levels = int(cur["fors_cta_levels"])
-        c.tree_split = int(bool(cur["tree_split"]))
+        c.tree_split = int(cur["tree_split"])
+        c.overlap = int(bool(cur["overlap"]))
         self._check(_lib.lib().hs_config_set(self._h, SET_INDEX[set_id], ctypes.byref(c)), "hs_config_set")
         return self.config(set_id)
 
@@ -377,7 +379,7 @@ class Engine:
         if n < 0:
             self._check(n, "hs_batch_info")
         return {"staged": int(v[0]), "shared_layers": int(v[1]), "fors_cta_levels": int(v[2]),
-                "tree_split": bool(v[3]), "shared_subtrees_built": int(v[4])}
+                "tree_split": int(v[3]), "shared_subtrees_built": int(v[4])}
 
     def launch_stats(self, reset: bool = True) -> dict:
         """Host-side batch launch latency: cudaGraphLaunch calls since the last reset."""

@@ -273,6 +273,9 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
     2. For each kernel every compiled SHA-256 path (engine.variants()) is timed;
        the fastest replaces 'native' only if it is faster by more than
        ``tie_tolerance`` (the reference's rule, tuner.py:206-218).
+    3. Sub-batches per graph (T) and stream overlap (FORS_Sign || TREE_Sign and
+       concurrent sub-batches, or one stream order) are timed end to end from
+       pinned host buffers at ``count`` messages.
     Returns the chosen config plus the timing table; the engine is left
     configured with it.
     """
@@ -337,20 +340,21 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
     out = PinnedBuffer(count * p.sig_bytes)
     stable = {}
     try:
-        for T in (1, 2, 3, 4, 6, 8):
-            engine.set_config(set_id, streams=T)
+        for T, ov in [(T, ov) for ov in (True, False) for T in (1, 2, 3, 4, 6, 8)]:
+            engine.set_config(set_id, streams=T, overlap=ov)
             engine.sign_into(set_id, blob, offs, count, out.ptr)
             runs = []
             for _ in range(reps):
                 t0 = time.perf_counter()
                 engine.sign_into(set_id, blob, offs, count, out.ptr)
                 runs.append(1e3 * (time.perf_counter() - t0))
-            stable[T] = _trimmed_mean(runs)
+            stable[T if ov else f"{T}/serial"] = _trimmed_mean(runs)
     finally:
         out.free()
     _synthetic(engine, set_id, count)
-    best_T = min(stable, key=stable.get)
-    engine.set_config(set_id, streams=best_T)
+    best_key = min(stable, key=stable.get)
+    best_T = int(str(best_key).split("/")[0])
+    engine.set_config(set_id, streams=best_T, overlap=not str(best_key).endswith("/serial"))
     return {"set": set_id, "count": count, "smem_optin": info["smem_optin"], "layouts": table,
             "best_layout": best, "cta_levels_ms": ltable, "variants": variants, "variant_ms": vtable,
             "streams_ms": stable,

@@ -65,10 +65,12 @@ def test_batch_sizes_and_graph_replay(eng, oracle_mod, count):
     assert all(eng.verify_batch("128f", sk[32:], msgs, first))
 
 
+@pytest.mark.parametrize("overlap", [True, False])
 @pytest.mark.parametrize("set_id", SETS)
-def test_chunked_multistream_mixed_keys(eng, oracle_mod, set_id):
+def test_chunked_multistream_mixed_keys(eng, oracle_mod, set_id, overlap):
     """hs_sign_batch over several chunks (chunk < count), 4 weighted sub-batches
-    per chunk, two keys, mixed opt_rand: every signature equals the oracle's."""
+    per chunk (FORS || TREE streams and concurrent sub-batches, or one stream
+    order), two keys, mixed opt_rand: every signature equals the oracle's."""
     p = derive(set_id)
     rng = random.Random(4242 + p.n)
     sks = [oracle_mod.keygen(set_id, rng.randbytes(3 * p.n)) for _ in range(2)]
@@ -79,7 +81,7 @@ def test_chunked_multistream_mixed_keys(eng, oracle_mod, set_id):
     eng.upload_keys(set_id, sks)
     base = eng.config(set_id)
     try:
-        eng.set_config(set_id, chunk=1024, streams=4)
+        eng.set_config(set_id, chunk=1024, streams=4, overlap=overlap)
         sigs, steps = eng.sign_batch(set_id, msgs, key_idx=kidx, opt_rand=opts, counts=True)
     finally:
         eng.set_config(set_id, **base)

@@ -100,11 +100,13 @@ def test_layouts_and_variants(eng, oracle_mod, set_id, variant, stash):
                "256f": [(1, 1, 0), (2, 2, 1), (1, 5, 1), (3, 6, 1)]}[set_id]
     try:
         for i, (nt, f, rx) in enumerate(layouts):
-            # alternate the split (chain grid + leaf grid) and fused TREE_Sign
+            # cycle the TREE_Sign shapes: chain + leaf + Merkle grids, fused,
+            # chain + leaf grid with warp-shuffle Merkle
+            split = (2, 0, 1, 2)[i]
             eng.set_config(set_id, fors_trees_per_set=nt, fors_sets_fused=f, fors_relax=bool(rx), wots_from_tree=stash,
                            variant={k: variant for k in ("FORS_Sign", "TREE_Sign", "WOTS_Sign", "host")},
-                           tree_split=(i % 2 == 0))
-            assert eng.sign_batch(set_id, msgs) == ref, (nt, f, rx, i % 2 == 0)
+                           tree_split=split)
+            assert eng.sign_batch(set_id, msgs) == ref, (nt, f, rx, split)
         assert eng.keygen_batch(set_id, [seed])[0] == sk  # keygen root kernel on this path
     finally:
         eng.set_config(set_id, **base)
@@ -146,14 +148,16 @@ def test_config_change_rebuilds_graph(eng, oracle_mod):
     base = eng.config(set_id)
     try:
         counts = {}
-        for split, lc in ((True, -1), (False, p.log_t), (True, -1)):
+        for split, lc in ((1, -1), (0, p.log_t), (1, -1), (2, -1)):
             eng.set_config(set_id, tree_split=split, fors_cta_levels=lc, streams=1, shared_layers=0)
             n0 = eng.launch_count
             assert eng.sign_batch(set_id, msgs) == ref, (split, lc)
             counts.setdefault((split, lc), []).append(eng.launch_count - n0)
-        # split TREE_Sign adds the leaf grid; leaves-only FORS adds log_t level grids
-        assert counts[(True, -1)][0] - counts[(False, p.log_t)][0] == 1 + p.log_t
-        assert counts[(True, -1)][0] == counts[(True, -1)][1]
+        # split TREE_Sign adds the leaf grid (and with 2 the Merkle grid);
+        # leaves-only FORS adds log_t level grids
+        assert counts[(1, -1)][0] - counts[(0, p.log_t)][0] == 1 + p.log_t
+        assert counts[(2, -1)][0] - counts[(1, -1)][0] == 1
+        assert counts[(1, -1)][0] == counts[(1, -1)][1]
     finally:
         eng.set_config(set_id, **base)
 

@@ -126,7 +126,7 @@ def test_shipped_tuned_config_is_loadable_and_in_range():
         b = row.b200
         assert all(0 <= v < n_paths for v in b["variant"].values()), (set_id, b["variant"])
         assert -1 <= b.get("fors_cta_levels", -1) <= derive(set_id).log_t
-        assert b.get("tree_split", True) in (True, False)
+        assert b.get("tree_split", 1) in (0, 1, 2)
 
 
 class _FakeSigner:
