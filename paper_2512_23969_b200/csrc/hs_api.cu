@@ -567,16 +567,21 @@ void sub_range(uint32_t count, int T, int j, uint32_t& first, uint32_t& cn) {
 // Multi-stream batch (the paper's m x T batching), one
 // graph per batch shape:
 //
-//   s0: [memset key_used] -> msg_prep(all) -> fork
-//   q0: [shared subtrees] ...................................-> sh
-//   qj: FORS_j -> T_k_j -> TREE_j -> (wait sh) -> WOTS_j -> done_j -> join
-//
-// Sub-batch j's stream qj has the j-th highest priority and the graph is
+// overlap = 1:
+//   s0:      [memset key_used] -> msg_prep(all) -> fork
+//   q0:      [shared subtrees] ...................................-> sh
+//   q(1+2j): TREE_j ............ (wait fjoin_j, sh) -> WOTS_j -> done_j -> join
+//   q(2+2j): FORS_j -> levels -> T_k_j -> fjoin_j
+// Sub-batch j's streams have the j-th highest priorities and the graph is
 // instantiated with per-node priorities, so the block scheduler drains
-// sub-batch 0 first while later ones fill the idle slots and the tail; each
-// sub-batch's signatures are complete (event done_j) while the others still
-// run, so their D2H copies (issued on ls[j] outside the graph) overlap the
-// remaining compute.  The shared-subtree kernel runs once for the whole batch.
+// sub-batch 0 first while later ones fill the idle slots and the tail.
+// overlap = 0: one stream order after msg_prep -- shared subtrees, then per
+// sub-batch FORS_j, TREE_j, WOTS_j -> done_j (no kernel concurrency; measured
+// faster for 192f/256f, whose large FORS CTAs slow co-resident chain blocks).
+// Either way each sub-batch's signatures are complete (event done_j) while
+// later sub-batches still compute, so their D2H copies (issued on ls[j]
+// outside the graph) overlap the remaining compute.  The shared-subtree
+// kernel runs once for the whole batch.
 cudaError_t enqueue_batch(hs_t* h, int set, uint32_t io_first, uint32_t count, int T, bool capture) {
   const hs_set_config& c = h->sets[set].cfg;
   const LaunchArgs all = make_args(h, set, io_first, 0, count);

@@ -12,9 +12,12 @@
 //   fors_level   one upper FORS level for the whole batch
 //   fors_pk      T_k over the k FORS roots (vexec.py:476-481)
 //   tree_chain   TREE_Sign part 1: one thread per WOTS chain (wots.py:42-65)
-//   tree_root    TREE_Sign part 2: one thread per hypertree leaf: T_len over
-//                the chain ends, warp-shuffle Merkle reduction
-//                (wots.py:119-143, vexec.py:492-551 / oracle.py:27-63)
+//   tree_leaf    TREE_Sign part 2: one thread per hypertree leaf: T_len over
+//                the chain ends (wots.py:119-143)
+//   tree_merkle  TREE_Sign part 3: one thread per subtree: Merkle levels,
+//                auth path, root (vexec.py:492-551 / oracle.py:27-63)
+//   tree_root    parts 2+3 in one grid with a warp-shuffle Merkle reduction
+//                (tree_split=1)
 //   tree_sign    fused TREE_Sign (thread = leaf runs its chains), tree_split=0
 //   shared_*     the top layers' subtrees, once per batch (both shapes)
 //   wots_gather  WOTS+_Sign from the chain nodes TREE_Sign recorded;
