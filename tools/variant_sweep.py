@@ -41,7 +41,7 @@ def main():
                     for v, name in enumerate(names):
                         var = dict(base["variant"])
                         var[kernel] = v
-                        eng.set_config(set_id, variant=var, wots_from_tree=True, tree_split=bool(ts))
+                        eng.set_config(set_id, variant=var, wots_from_tree=True, tree_split=int(ts))
                         res.setdefault(key, {})[name] = round(
                             _trimmed_mean(_kernel_ms(eng, set_id, a.count, kernel, a.reps)), 4)
         finally:
