@@ -230,3 +230,59 @@ def test_multi_engine_two_handles_one_device(eng, oracle_mod):
     assert got == [ref[i] for i in sub]
     assert all(hs.verify_batch([msgs[i] for i in sub], got, [k.public() for k in keys], p,
                                key_idx=[int(kidx[i]) for i in sub], devices=[0, 0]))
+
+
+def test_concurrent_public_calls_different_keys(eng, oracle_mod):
+    """The reference's sign() is a pure function that callers use from many
+    threads (sigcore.py:139-178).  Six threads share the process-wide engine,
+    each with its own key and its own per-call FORS layout / SHA-path
+    overrides, interleaving sign_batch and sign: every signature must be the
+    oracle's under the caller's key, and the engine's configuration must come
+    back unchanged (the key upload, overrides, sign and restore form one
+    critical section, engine.Engine.lock)."""
+    import threading
+
+    set_id = "128f"
+    p = derive(set_id)
+    rng = random.Random(2024)
+    keys = [hs.keygen(set_id, rng.randbytes(3 * p.n)) for _ in range(6)]
+    work = [[rng.randbytes(rng.choice([0, 31, 32, 100])) for _ in range(9)] for _ in keys]
+    fusions = [None, type("F", (), {"trees_per_set": 3, "sets_fused": 1})(), None,
+               type("F", (), {"trees_per_set": 1, "sets_fused": 11})(), None, None]
+
+    class Sel:  # duck-typed reference BackendSelection (backends.py:201-257)
+        def __init__(self, v):
+            self.v = v
+
+        def get(self, kernel, set_id):
+            return self.v
+
+    sels = [None, None, Sel("baseline"), None, Sel("tuned"), None]
+    base = eng.config(set_id)
+    got: dict = {}
+    errors: list = []
+    start = threading.Barrier(len(keys))
+
+    def worker(t):
+        try:
+            start.wait()
+            out = []
+            for r in range(3):
+                if r == 1:
+                    out += [hs.sign(m, keys[t], set_id, fusion=fusions[t], selection=sels[t]) for m in work[t][:3]]
+                else:
+                    out += hs.sign_batch(work[t], keys[t], set_id, fusion=fusions[t], selection=sels[t])
+            got[t] = out
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(len(keys))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    for t, k in enumerate(keys):
+        ref = [oracle_mod.sign(set_id, k.to_bytes(), m) for m in work[t]]
+        assert got[t] == ref + ref[:3] + ref, f"thread {t}"
+    assert eng.config(set_id) == base
