@@ -102,7 +102,16 @@ typedef struct {
                                  and sub-batches run concurrently (priority
                                  ordered); 0: every kernel of the batch in one
                                  stream order -- sub-batches then only
-                                 pipeline the signatures' D2H copies         */
+                                 pipeline the signatures' D2H copies; N >= 2:
+                                 streams for graphs of at most N messages,
+                                 one stream order above (small batches leave
+                                 the GPU idle without the concurrency)       */
+  int32_t fors_small_batch;   /* graphs of at most this many messages run
+                                 FORS_Sign with one tree per CTA (N_tree = F
+                                 = 1; Relax and fors_cta_levels as set):
+                                 k CTAs per message spread over the SMs
+                                 instead of a few wide CTAs; 0 = off.  Bytes
+                                 are unchanged (layouts never change them)   */
 } hs_set_config;
 
 HS_API int hs_open(int device, hs_t **out);

@@ -51,6 +51,7 @@ class SetConfig(ctypes.Structure):
         ("fors_cta_levels", ctypes.c_int32),
         ("tree_split", ctypes.c_int32),
         ("overlap", ctypes.c_int32),
+        ("fors_small_batch", ctypes.c_int32),
     ]
 
 

@@ -113,7 +113,8 @@ class TuningConfig:
                                   stacklevel=2)
             kw = {}
             for key in ("fors_trees_per_set", "fors_sets_fused", "fors_relax", "wots_from_tree", "chunk", "streams",
-                        "shared_layers", "shared_auto", "fors_cta_levels", "tree_split", "overlap"):
+                        "shared_layers", "shared_auto", "fors_cta_levels", "tree_split", "overlap",
+                        "fors_small_batch"):
                 if key in b:
                     kw[key] = b[key]
             if "variant" in b:
@@ -133,6 +134,7 @@ class TuningConfig:
                 "wots_from_tree": e["wots_from_tree"], "chunk": e["chunk"], "streams": e["streams"],
                 "shared_layers": e["shared_layers"], "shared_auto": e["shared_auto"],
                 "fors_cta_levels": e["fors_cta_levels"], "tree_split": e["tree_split"], "overlap": e["overlap"],
+                "fors_small_batch": e["fors_small_batch"],
             }
             cfg.sets[set_id].backends = {k: "tuned" if e["variant"][k] else "baseline" for k in KERNELS}
         return cfg

@@ -126,7 +126,11 @@ hs_set_config default_config(int set) {
   c.shared_auto = 1;
   c.fors_cta_levels = -1;
   c.tree_split = 2;
-  c.overlap = 1;
+  // streams for graphs of at most this many messages (1 = always): measured
+  // crossover on B200, profiles/r02y_overlap_crossover.txt
+  static const int ov[3] = {1, 1536, 8192}, small[3] = {64, 64, 0};
+  c.overlap = ov[set];
+  c.fors_small_batch = small[set];
   return c;
 }
 
@@ -306,7 +310,8 @@ int check_layout(hs_t* h, int set, const hs_set_config& c) {
     return fail(h, HS_E_CONFIG, "shared_layers must be in 0..%d for this set", shared_max(set));
   if (c.shared_auto != 0 && c.shared_auto != 1) return fail(h, HS_E_CONFIG, "shared_auto must be 0 or 1");
   if (c.tree_split < 0 || c.tree_split > 2) return fail(h, HS_E_CONFIG, "tree_split must be 0, 1 or 2");
-  if (c.overlap != 0 && c.overlap != 1) return fail(h, HS_E_CONFIG, "overlap must be 0 or 1");
+  if (c.overlap < 0) return fail(h, HS_E_CONFIG, "overlap must be 0, 1 or a message count >= 2");
+  if (c.fors_small_batch < 0) return fail(h, HS_E_CONFIG, "fors_small_batch must be >= 0");
   if (c.fors_cta_levels < -1 || c.fors_cta_levels > I.log_t)
     return fail(h, HS_E_CONFIG, "fors_cta_levels must be -1 (auto) or in 0..%d", I.log_t);
   return HS_OK;
@@ -354,6 +359,23 @@ int fors_cta_levels(int set, const hs_set_config& c, uint32_t count) {
   return std::max(lowest, std::min(c.fors_cta_levels, I.log_t));
 }
 
+// The execution shape of one batch graph of `count` messages: the set's
+// config with the batch-size rules resolved.  Small graphs leave most SMs
+// idle, so (a) FORS_Sign runs one tree per CTA (k CTAs per message instead of
+// a few wide ones whose lanes walk several trees in passes) and (b) the FORS /
+// TREE / shared-subtree branches run concurrently; large graphs keep the
+// tuned layout and, where concurrency measured slower (192f, 256f at 16,384),
+// one stream order.  Bytes never depend on the shape.
+hs_set_config batch_config(const hs_set_config& c, uint32_t count) {
+  hs_set_config b = c;
+  if (c.fors_small_batch > 0 && count <= (uint32_t)c.fors_small_batch) {
+    b.fors_trees_per_set = 1;
+    b.fors_sets_fused = 1;
+  }
+  b.overlap = (c.overlap == 1 || (c.overlap > 1 && count <= (uint32_t)c.overlap)) ? 1 : 0;
+  return b;
+}
+
 // words of fors_nodes[b]: buffer 0 holds levels Lc, Lc+2, ..., buffer 1 Lc+1, ...
 size_t fors_node_words(int set, const hs_set_config& c, uint32_t count, int b) {
   const SetInfo& I = kInfo[set];
@@ -371,7 +393,8 @@ size_t chain_end_words(int set, uint32_t count) {
 // whose per-message work buffers start at work_first (the message's index in
 // its chunk).  Message offsets stay absolute into the staged blob; every
 // per-message buffer is offset, so sub-batches are independent launches.
-LaunchArgs make_args(hs_t* h, int set, uint32_t io_first, uint32_t work_first, uint32_t count) {
+LaunchArgs make_args(hs_t* h, int set, const hs_set_config& c, uint32_t io_first, uint32_t work_first,
+                     uint32_t count) {
   const uint32_t first = work_first;
   const SetInfo& I = kInfo[set];
   SetState& St = h->sets[set];
@@ -392,10 +415,10 @@ LaunchArgs make_args(hs_t* h, int set, uint32_t io_first, uint32_t work_first, u
   a.indices = B.idx + (size_t)first * I.k;
   a.roots = B.roots + (size_t)first * (I.d + 1) * 8;
   a.fors_roots = B.froots + (size_t)first * I.k * 8;
-  a.fors_trees_per_set = St.cfg.fors_trees_per_set;
-  a.fors_sets_fused = St.cfg.fors_sets_fused;
-  a.fors_relax = St.cfg.fors_relax;
-  a.fors_cta_levels = fors_cta_levels(set, St.cfg, count);
+  a.fors_trees_per_set = c.fors_trees_per_set;
+  a.fors_sets_fused = c.fors_sets_fused;
+  a.fors_relax = c.fors_relax;
+  a.fors_cta_levels = fors_cta_levels(set, c, count);
   if (a.fors_cta_levels < I.log_t) {
     for (int b = 0; b < 2; b++)
       a.fors_nodes[b] = B.fnodes[b] + (size_t)first * I.k * ((size_t)I.t >> (a.fors_cta_levels + b)) * (I.n / 4);
@@ -583,8 +606,8 @@ void sub_range(uint32_t count, int T, int j, uint32_t& first, uint32_t& cn) {
 // outside the graph) overlap the remaining compute.  The shared-subtree
 // kernel runs once for the whole batch.
 cudaError_t enqueue_batch(hs_t* h, int set, uint32_t io_first, uint32_t count, int T, bool capture) {
-  const hs_set_config& c = h->sets[set].cfg;
-  const LaunchArgs all = make_args(h, set, io_first, 0, count);
+  const hs_set_config c = batch_config(h->sets[set].cfg, count);
+  const LaunchArgs all = make_args(h, set, c, io_first, 0, count);
   auto rec = [&](cudaEvent_t ev, cudaStream_t s) {
     return capture ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal) : cudaEventRecord(ev, s);
   };
@@ -608,7 +631,7 @@ cudaError_t enqueue_batch(hs_t* h, int set, uint32_t io_first, uint32_t count, i
       uint32_t first, cn;
       sub_range(count, T, j, first, cn);
       if (cn == 0) break;
-      const LaunchArgs a = make_args(h, set, io_first + first, first, cn);
+      const LaunchArgs a = make_args(h, set, c, io_first + first, first, cn);
       TRY(enqueue_fors(set, c, a, q, kernels));
       TRY(enqueue_tree(set, c, a, q, kernels));
       TRY(launch(set, a.stash ? K_WOTS_GATHER : K_WOTS, c.variant[2], a, q));
@@ -631,7 +654,7 @@ cudaError_t enqueue_batch(hs_t* h, int set, uint32_t io_first, uint32_t count, i
     uint32_t first, cn;
     sub_range(count, T, j, first, cn);
     if (cn == 0) break;
-    const LaunchArgs a = make_args(h, set, io_first + first, first, cn);
+    const LaunchArgs a = make_args(h, set, c, io_first + first, first, cn);
     // TREE_j on priority 1+2j, FORS_j just below it: FORS_j's short CTAs fill
     // the SMs TREE_j drains before TREE_{j+1} claims them, and the last
     // sub-batch's FORS fills the final tail.
@@ -721,7 +744,7 @@ int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nu
   for (int j = 0; j < kMaxStreams; j++) CUDA_TRY(h, cudaStreamWaitEvent(h->s0, h->d2h_done[slot][j], 0));
   if (mode == 1) {  // serialised kernels with per-kernel events (roofline timing): one chunk
     if (count > chunk) return fail(h, HS_E_USAGE, "serialised timing runs at most one chunk (%u messages)", chunk);
-    CUDA_TRY(h, enqueue(h, set, make_args(h, set, 0, 0, count), false, true));
+    CUDA_TRY(h, enqueue(h, set, make_args(h, set, batch_config(St.cfg, count), 0, 0, count), false, true));
     CUDA_TRY(h, cudaEventRecord(h->compute_done[slot], h->s0));
     if (fetch_to) CUDA_TRY(h, cudaMemcpyAsync(fetch_to, S.sigs, count * sb, cudaMemcpyDeviceToHost, h->s0));
     if (wsteps_to) CUDA_TRY(h, cudaMemcpyAsync(wsteps_to, S.wsteps, count * 4, cudaMemcpyDeviceToHost, h->s0));
@@ -1275,7 +1298,9 @@ int hs_batch_info(hs_t* h, int set, int32_t* out, int cap) {
     CUDA_TRY(h, cudaMemcpy(f.data(), B.key_used + St.nkeys, f.size(), cudaMemcpyDeviceToHost));
     for (uint8_t x : f) built += x != 0;
   }
-  const int32_t v[5] = {(int32_t)St.staged, St.shared_eff, fors_cta_levels(set, St.cfg, St.staged), St.cfg.tree_split, built};
+  const uint32_t graph_count = std::min<uint32_t>(St.staged, (uint32_t)std::max(1, St.cfg.chunk));
+  const int32_t v[5] = {(int32_t)St.staged, St.shared_eff,
+                        fors_cta_levels(set, batch_config(St.cfg, graph_count), graph_count), St.cfg.tree_split, built};
   const int n = std::min(cap, 5);
   for (int i = 0; i < n; i++) out[i] = v[i];
   return n;
@@ -1362,15 +1387,28 @@ int time_stage(hs_t* h, int set, uint32_t count, int stage, int reps, std::vecto
   return HS_OK;
 }
 
+// Device time (ms, CUDA events inside the graph) of the staged batch as one graph launch.
+int time_graph(hs_t* h, int set, uint32_t count, int reps, std::vector<float>& out) {
+  out.clear();
+  for (int r = 0; r < reps; r++) {
+    if (int rc = run_batch(h, set, count, 0); rc != HS_OK) return rc;
+    float ms[5];
+    if (hs_timings(h, ms, 5) < 1) return fail(h, HS_E_CUDA, "tune: timing events");
+    out.push_back(ms[0]);
+  }
+  return HS_OK;
+}
+
 std::string cfg_json(const hs_set_config& c) {
   char b[512];
   snprintf(b, sizeof b,
            "{\"fors_trees_per_set\": %d, \"fors_sets_fused\": %d, \"fors_relax\": %d, \"variant\": [%d, %d, %d, %d], "
            "\"use_graph\": %d, \"chunk\": %d, \"wots_from_tree\": %d, \"streams\": %d, \"shared_layers\": %d, "
-           "\"shared_auto\": %d, \"fors_cta_levels\": %d, \"tree_split\": %d, \"overlap\": %d}",
+           "\"shared_auto\": %d, \"fors_cta_levels\": %d, \"tree_split\": %d, \"overlap\": %d, "
+           "\"fors_small_batch\": %d}",
            c.fors_trees_per_set, c.fors_sets_fused, c.fors_relax, c.variant[0], c.variant[1], c.variant[2],
            c.variant[3], c.use_graph, c.chunk, c.wots_from_tree, c.streams, c.shared_layers, c.shared_auto,
-           c.fors_cta_levels, c.tree_split, c.overlap);
+           c.fors_cta_levels, c.tree_split, c.overlap, c.fors_small_batch);
   return b;
 }
 
@@ -1512,6 +1550,61 @@ int hs_tune(hs_t* h, int set, uint32_t count, int32_t top, int32_t reps, char* j
   js += "}";
   c.streams = best_T;
   c.overlap = best_ov;
+  // 4. batch-size rules (batch_config), graph device time on smaller batches
+  //    of the same messages: (a) when one stream order won at `count`, the
+  //    largest of count/2, count/4, ... (>= 16) at which the concurrent
+  //    branches are faster becomes the overlap threshold; (b) one FORS tree
+  //    per CTA is kept for graphs up to the largest of 16, 64, 256 messages at
+  //    which it is faster than the tuned layout by more than 2 %.
+  auto graph_ms = [&](uint32_t n, double& ms) -> int {
+    if (int r = hs_config_set(h, set, &c); r != HS_OK) return r;
+    if (int r = stage_inputs(h, set, 0, msgs.data(), offs.data(), nullptr, nullptr, 0, n, false); r != HS_OK) return r;
+    if (int r = time_graph(h, set, n, 2, t); r != HS_OK) return r;  // warm-up, graph capture
+    if (int r = time_graph(h, set, n, reps, t); r != HS_OK) return r;
+    ms = trimmed_mean(t);
+    return HS_OK;
+  };
+  c.fors_small_batch = 0;
+  js += ", \"overlap_ms\": {";
+  if (best_ov == 0) {
+    bool firstk = true;
+    for (uint32_t n = count / 2; n >= 16; n /= 2) {
+      double m1, m0;
+      c.overlap = 1;
+      if (int r = graph_ms(n, m1); r != HS_OK) return r;
+      c.overlap = 0;
+      if (int r = graph_ms(n, m0); r != HS_OK) return r;
+      char b[96];
+      snprintf(b, sizeof b, "%s\"%u\": [%.4f, %.4f]", firstk ? "" : ", ", n, m1, m0);
+      js += b;
+      firstk = false;
+      if (m1 < m0) {
+        c.overlap = n >= 2 ? (int)n : 1;
+        break;
+      }
+    }
+  }
+  js += "}, \"small_batch_ms\": {";
+  const int small_ov = c.overlap;
+  int small = 0;
+  for (uint32_t n : {16u, 64u, 256u}) {
+    if (n > count) break;
+    double tuned, one_tree;
+    c.fors_small_batch = 0;
+    if (int r = graph_ms(n, tuned); r != HS_OK) return r;
+    c.fors_small_batch = (int)n;
+    if (int r = graph_ms(n, one_tree); r != HS_OK) return r;
+    char b[96];
+    snprintf(b, sizeof b, "%s\"%u\": [%.4f, %.4f]", n == 16 ? "" : ", ", n, tuned, one_tree);
+    js += b;
+    if (!(one_tree < tuned * 0.98)) break;
+    small = (int)n;
+  }
+  js += "}";
+  c.fors_small_batch = small;
+  c.overlap = small_ov;
+  if (int r = stage_inputs(h, set, 0, msgs.data(), offs.data(), nullptr, nullptr, 0, count, false); r != HS_OK)
+    return r;
   c.chunk = base.chunk;
   if (int r2 = hs_config_set(h, set, &c); r2 != HS_OK) return r2;
   js += ", \"config\": " + cfg_json(c) + "}";

@@ -102,6 +102,9 @@ struct LaunchArgs {
   uint32_t* wots_steps;
 };
 
+// L1 prefetch hint (latency-bound single-thread loops: T_len, T_k, Merkle levels)
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 __device__ __forceinline__ uint64_t shr64(uint64_t x, int s) { return s >= 64 ? 0ull : (x >> s); }
 
 __device__ __forceinline__ void store_be(uint8_t* p, uint32_t w) { *reinterpret_cast<uint32_t*>(p) = bswap32(w); }
@@ -213,7 +216,7 @@ __global__ void msg_prep_kernel(LaunchArgs a) {
 #pragma unroll
     for (int j = 9; j < 15; j++) W[j] = 0;
     W[15] = (64 + 32) * 8;
-    compress_compact<V>(R, W);
+    compress_prep<V>(R, W);
   }
   uint8_t* sig = a.sigs + (size_t)i * Pr::sig_bytes;
   store_node<NW>(sig, R);
@@ -596,6 +599,11 @@ __global__ void __launch_bounds__(kTreeBlock) tree_leaf_kernel(LaunchArgs a) {
     uint32_t W[16];
 #pragma unroll
     for (int j = 0; j < 16; j++) W[j] = tlen_word<M>(16u * b + j, aw, e, (64u + total) * 8u, 16u * nblk - 1u);
+    // the next block's chain-end words (e[16b+10 .. 16b+26]) are requested
+    // while this block compresses: a lone leaf thread (small batches) no
+    // longer waits one L2 round trip per block
+    if (16u * b + 26u < (uint32_t)M) prefetch_l1(e + 16u * b + 26u);
+    if (16u * b + 10u < (uint32_t)M) prefetch_l1(e + 16u * b + 10u);
     compress<V>(node, W);
   }
   // the leaf replaces the head of its own (consumed) chain-end record, where
@@ -610,10 +618,11 @@ __global__ void __launch_bounds__(kTreeBlock) tree_leaf_kernel(LaunchArgs a) {
 }
 
 // TREE_Sign part 3: thread = (message, layer) reduces its subtree's leaves
-// (treehash, oracle.py:27-63 / vexec.py:518-551) level by level, in place over
-// the leaves' records in chain_ends (node j of level L overwrites the record
-// of leaf j: its children 2j, 2j+1 are read first), storing the auth path
-// nodes of levels 1..hp-1 and the root.  One thread per subtree keeps every
+// (treehash, oracle.py:27-63 / vexec.py:518-551) level by level -- level 1
+// from the leaves tree_leaf_kernel left at the heads of their chain-end
+// records, the levels above in place in a thread-local buffer (node j of level
+// L replaces node j of level L-1 after its children 2j, 2j+1 are read) --
+// storing the auth path nodes of levels 1..hp-1 and the root.  One thread per subtree keeps every
 // lane busy at every level; reducing inside tree_root with warp shuffles left
 // 1/2, 3/4, 7/8 of a subtree's lanes idle at levels 1, 2, 3.
 template <int S, class V>
@@ -634,9 +643,16 @@ __global__ void __launch_bounds__(kTreeBlock) tree_merkle_kernel(LaunchArgs a) {
   uint32_t mid[8];
 #pragma unroll
   for (int j = 0; j < 8; j++) mid[j] = K.thash_mid[j];
-  uint32_t* base = a.chain_ends + gid * (uint64_t)Pr::leaves * M;
+  const uint32_t* base = a.chain_ends + gid * (uint64_t)Pr::leaves * M;
   uint8_t* auth = a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_ht + (size_t)layer * Pr::layer_bytes +
                   Pr::wots_sig_bytes;
+  // every leaf head is requested up front (one L1 prefetch per record), so the
+  // level-1 loads do not each wait a full L2 round trip behind the previous H
+#pragma unroll
+  for (int i = 0; i < Pr::leaves; i++) prefetch_l1(base + (size_t)i * M);
+  // levels >= 1 live in this thread's local memory (L1-resident: a store and
+  // the later load of the same thread never round-trip through L2)
+  uint32_t lv[Pr::leaves / 2][NW];
   uint32_t node[8];
 #pragma unroll 1
   for (int lvl = 1; lvl <= Pr::hp; lvl++) {
@@ -645,15 +661,17 @@ __global__ void __launch_bounds__(kTreeBlock) tree_merkle_kernel(LaunchArgs a) {
 #pragma unroll 1
     for (uint32_t j = 0; j < per; j++) {
       uint32_t m[2 * NW];
-      const uint32_t* c0 = base + (size_t)(2 * j) * M;
-      const uint32_t* c1 = c0 + M;
+      if (lvl == 1) {
 #pragma unroll
-      for (int w = 0; w < NW; w++) { m[w] = c0[w]; m[NW + w] = c1[w]; }
+        for (int w = 0; w < NW; w++) { m[w] = base[(size_t)(2 * j) * M + w]; m[NW + w] = base[(size_t)(2 * j + 1) * M + w]; }
+      } else {
+#pragma unroll
+        for (int w = 0; w < NW; w++) { m[w] = lv[2 * j][w]; m[NW + w] = lv[2 * j + 1][w]; }
+      }
       thash_reg<V, 2 * NW>(node, mid, make_adrs(layer, tree, ADDR_HASHTREE, 0, (uint32_t)lvl, j), m);
       if (lvl < Pr::hp && j == sib) store_node<NW>(auth + lvl * Pr::n, node);
-      uint32_t* d = base + (size_t)j * M;
 #pragma unroll
-      for (int w = 0; w < NW; w++) d[w] = node[w];
+      for (int w = 0; w < NW; w++) lv[j][w] = node[w];
     }
   }
   uint32_t* r = a.roots + ((size_t)msg * (Pr::d + 1) + layer + 1) * 8;
@@ -1177,8 +1195,11 @@ __global__ void __launch_bounds__(kSmallBlock) fors_pk_kernel(LaunchArgs a) {
   TStream<V> ts;
   ts.begin(mid, make_adrs(0, pl.tree, ADDR_FORS_ROOTS, pl.leaf, 0, 0), &tbuf[threadIdx.x], kSmallBlock);
   const uint32_t* fr = a.fors_roots + (size_t)i * Pr::k * 8;
+#pragma unroll
+  for (int g = 0; g < 8; g += 4) prefetch_l1(fr + g * 8);
 #pragma unroll 1
   for (int g = 0; g < Pr::k; g++) {
+    if (g % 4 == 0 && g + 8 < Pr::k) prefetch_l1(fr + (g + 8) * 8);  // two 128-B lines (8 roots) ahead
     uint32_t x[NW];
 #pragma unroll
     for (int j = 0; j < NW; j++) x[j] = fr[g * 8 + j];

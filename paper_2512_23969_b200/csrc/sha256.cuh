@@ -308,6 +308,32 @@ __device__ __noinline__ void compress_compact(uint32_t st[8], const uint32_t Win
   st[0] += a; st[1] += b; st[2] += c; st[3] += d; st[4] += e; st[5] += f; st[6] += g; st[7] += h;
 }
 
+// The same compression fully unrolled but out of line: one copy of the code
+// for every call site of a latency-bound single-thread hash chain.  A lone
+// warp runs it in ~3000 cycles against ~4400 for compress_compact, whose
+// round loop and constant-memory K reads sit on the critical path
+// (tools/lat_probe.cu, profiles/r02t_lat_probe.txt).
+template <class V>
+__device__ __noinline__ void compress_ool(uint32_t st[8], const uint32_t Win[16]) {
+  uint32_t W[16];
+#pragma unroll
+  for (int j = 0; j < 16; j++) W[j] = Win[j];
+  compress<V>(st, W);
+}
+// message preparation / verify prologue compression: HS_PREP_UNROLLED=0
+// restores the compact form
+#ifndef HS_PREP_UNROLLED
+#define HS_PREP_UNROLLED 1
+#endif
+template <class V>
+__device__ __forceinline__ void compress_prep(uint32_t st[8], const uint32_t W[16]) {
+#if HS_PREP_UNROLLED
+  compress_ool<V>(st, W);
+#else
+  compress_compact<V>(st, W);
+#endif
+}
+
 // Rounds [0, R) only (no schedule expansion needed while R <= 16).
 template <class V, int R>
 __device__ __forceinline__ void rounds_prefix(uint32_t s[8], const uint32_t* W) {
@@ -632,7 +658,7 @@ __device__ __forceinline__ void sha_prefix_msg(uint32_t st[8], uint64_t absorbed
       W[j] = k < P ? pre[k < P ? k : 0] : msg_word(m, mlen, (uint64_t)(k - P));
     }
     if ((uint64_t)b == nblk - 1) { W[14] = (uint32_t)(bits >> 32); W[15] = (uint32_t)bits; }
-    compress_compact<V>(st, W);
+    compress_prep<V>(st, W);
   }
 #pragma unroll 1
   for (uint64_t b = PB; b < nblk; b++) {
@@ -640,7 +666,7 @@ __device__ __forceinline__ void sha_prefix_msg(uint32_t st[8], uint64_t absorbed
 #pragma unroll
     for (int j = 0; j < 16; j++) W[j] = msg_word(m, mlen, 16 * b + j - P);
     if (b == nblk - 1) { W[14] = (uint32_t)(bits >> 32); W[15] = (uint32_t)bits; }
-    compress_compact<V>(st, W);
+    compress_prep<V>(st, W);
   }
 }
 
@@ -671,7 +697,7 @@ __device__ __forceinline__ void sha_prefix_words(uint32_t st[8], uint64_t absorb
       W[j] = k < P ? pre[k < P ? k : 0] : (k - P < 17 ? mw[k - P < 17 ? k - P : 0] : 0u);
     }
     if ((uint32_t)b == nblk - 1) { W[14] = (uint32_t)(bits >> 32); W[15] = (uint32_t)bits; }
-    compress_compact<V>(st, W);
+    compress_prep<V>(st, W);
   }
 }
 

@@ -130,7 +130,8 @@ class Engine:
             "shared_auto": bool(c.shared_auto),
             "fors_cta_levels": c.fors_cta_levels,
             "tree_split": int(c.tree_split),
-            "overlap": bool(c.overlap),
+            "overlap": int(c.overlap),
+            "fors_small_batch": int(c.fors_small_batch),
         }
 
     def set_config(self, set_id: str, **kw) -> dict:
@@ -156,7 +157,8 @@ class Engine:
         c.shared_auto = int(bool(cur["shared_auto"]))
         c.fors_cta_levels = int(cur["fors_cta_levels"])
         c.tree_split = int(cur["tree_split"])
-        c.overlap = int(bool(cur["overlap"]))
+        c.overlap = int(cur["overlap"])
+        c.fors_small_batch = int(cur["fors_small_batch"])
         self._check(_lib.lib().hs_config_set(self._h, SET_INDEX[set_id], ctypes.byref(c)), "hs_config_set")
         return self.config(set_id)
 

@@ -94,8 +94,10 @@ def _apply_overrides(eng, p, fusion, relax, selection) -> dict | None:
     before = eng.config(p.id)
     kw = {}
     if fusion is not None:
+        # an explicit layout is run as given, whatever the batch size
         kw["fors_trees_per_set"] = int(fusion.trees_per_set)
         kw["fors_sets_fused"] = int(fusion.sets_fused)
+        kw["fors_small_batch"] = 0
     if relax is not None:
         kw["fors_relax"] = bool(getattr(relax, "enabled", relax))
     if selection is not None:

@@ -276,6 +276,9 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
     3. Sub-batches per graph (T) and stream overlap (FORS_Sign || TREE_Sign and
        concurrent sub-batches, or one stream order) are timed end to end from
        pinned host buffers at ``count`` messages.
+    4. The batch-size rules: the overlap threshold below ``count`` (when one
+       stream order won) and the largest graph that runs FORS_Sign with one
+       tree per CTA (``fors_small_batch``), from graph device times.
     Returns the chosen config plus the timing table; the engine is left
     configured with it.
     """
@@ -351,11 +354,43 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
             stable[T if ov else f"{T}/serial"] = _trimmed_mean(runs)
     finally:
         out.free()
-    _synthetic(engine, set_id, count)
     best_key = min(stable, key=stable.get)
     best_T = int(str(best_key).split("/")[0])
-    engine.set_config(set_id, streams=best_T, overlap=not str(best_key).endswith("/serial"))
+    best_ov = not str(best_key).endswith("/serial")
+    engine.set_config(set_id, streams=best_T, overlap=best_ov, fors_small_batch=0)
+    # 4. batch-size rules (the engine's batch_config), graph device time on
+    #    smaller batches: (a) when one stream order won at `count`, the largest
+    #    of count/2, count/4, ... (>= 16) at which the concurrent branches are
+    #    faster becomes the overlap threshold; (b) one FORS tree per CTA is kept
+    #    for graphs up to the largest of 16, 64, 256 messages at which it beats
+    #    the tuned layout by more than tie_tolerance.
+    def graph_ms(n: int, **kw) -> float:
+        engine.set_config(set_id, **kw)
+        _synthetic(engine, set_id, n)
+        engine.bench_run(set_id, n, 2, 0)
+        return _trimmed_mean(engine.bench_run(set_id, n, reps, 0))
+
+    otable, small_table = {}, {}
+    if not best_ov:
+        n = count // 2
+        while n >= 16:
+            otable[n] = (graph_ms(n, overlap=1), graph_ms(n, overlap=0))
+            if otable[n][0] < otable[n][1]:
+                engine.set_config(set_id, overlap=n)
+                break
+            engine.set_config(set_id, overlap=0)
+            n //= 2
+    small = 0
+    for n in (16, 64, 256):
+        if n > count:
+            break
+        small_table[n] = (graph_ms(n, fors_small_batch=0), graph_ms(n, fors_small_batch=n))
+        if not small_table[n][1] < small_table[n][0] * (1 - tie_tolerance):
+            break
+        small = n
+    engine.set_config(set_id, fors_small_batch=small)
+    _synthetic(engine, set_id, count)
     return {"set": set_id, "count": count, "smem_optin": info["smem_optin"], "layouts": table,
             "best_layout": best, "cta_levels_ms": ltable, "variants": variants, "variant_ms": vtable,
-            "streams_ms": stable,
+            "streams_ms": stable, "overlap_ms": otable, "small_batch_ms": small_table,
             "config": engine.config(set_id)}

@@ -105,7 +105,7 @@ def test_layouts_and_variants(eng, oracle_mod, set_id, variant, stash):
             split = (2, 0, 1, 2)[i]
             eng.set_config(set_id, fors_trees_per_set=nt, fors_sets_fused=f, fors_relax=bool(rx), wots_from_tree=stash,
                            variant={k: variant for k in ("FORS_Sign", "TREE_Sign", "WOTS_Sign", "host")},
-                           tree_split=split)
+                           tree_split=split, fors_small_batch=0)  # run the layout as given
             assert eng.sign_batch(set_id, msgs) == ref, (nt, f, rx, split)
         assert eng.keygen_batch(set_id, [seed])[0] == sk  # keygen root kernel on this path
     finally:
@@ -129,7 +129,7 @@ def test_fors_upper_levels_split(eng, oracle_mod, set_id):
                                                            int(base["fors_relax"]))):
             for lc in sorted({-1, 0, 1, 2, p.log_t - 1, p.log_t}):
                 eng.set_config(set_id, fors_trees_per_set=nt, fors_sets_fused=f, fors_relax=bool(rx),
-                               fors_cta_levels=lc)
+                               fors_cta_levels=lc, fors_small_batch=0)
                 assert eng.sign_batch(set_id, msgs) == ref, (nt, f, rx, lc)
     finally:
         eng.set_config(set_id, **base)
@@ -315,3 +315,28 @@ def test_api_roundtrip_golden(eng, golden):
     assert sig == (GOLDEN_DIR / "sig_192f_zero.bin").read_bytes()
     assert hs.verify(bytes(32), sig, sk.public(), "192f")
     assert not hs.verify(b"\x01" + bytes(31), sig, sk.public(), "192f")
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_batch_size_rules(eng, oracle_mod, set_id):
+    """The batch-size rules of the engine (batch_config): graphs of at most
+    fors_small_batch messages run FORS_Sign with one tree per CTA, graphs of
+    at most `overlap` (>= 2) messages run the FORS / TREE / shared branches
+    concurrently, larger ones in one stream order.  Counts on both sides of
+    each threshold, with Relax on and off, sign the oracle's bytes."""
+    p = derive(set_id)
+    rng = random.Random(4242)
+    sks = [oracle_mod.keygen(set_id, rng.randbytes(3 * p.n)) for _ in range(2)]
+    msgs = [rng.randbytes(rng.choice([0, 32, 90])) for _ in range(21)]
+    kidx = [rng.randrange(2) for _ in msgs]
+    ref, _ = oracle_mod.sign_many(set_id, b"".join(sks), kidx, msgs)
+    eng.upload_keys(set_id, sks)
+    base = eng.config(set_id)
+    try:
+        for relax in (False, True):
+            for small, ov in ((20, 0), (21, 20), (0, 21), (21, 1), (64, 0)):
+                eng.set_config(set_id, fors_relax=relax, fors_small_batch=small, overlap=ov, streams=1)
+                for n in (1, 20, 21):
+                    assert eng.sign_batch(set_id, msgs[:n], key_idx=kidx[:n]) == ref[:n], (relax, small, ov, n)
+    finally:
+        eng.set_config(set_id, **base)
