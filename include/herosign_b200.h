@@ -112,6 +112,11 @@ typedef struct {
                                  k CTAs per message spread over the SMs
                                  instead of a few wide CTAs; 0 = off.  Bytes
                                  are unchanged (layouts never change them)   */
+  int32_t tree_small_batch;   /* graphs of at most this many messages run a
+                                 tree_split 2 config as tree_split 1: the
+                                 subtree's Merkle levels as warp-shuffle
+                                 combines (hp H's deep) instead of one thread
+                                 walking all leaves-1 H's; 0 = off           */
 } hs_set_config;
 
 HS_API int hs_open(int device, hs_t **out);

@@ -52,6 +52,7 @@ class SetConfig(ctypes.Structure):
         ("tree_split", ctypes.c_int32),
         ("overlap", ctypes.c_int32),
         ("fors_small_batch", ctypes.c_int32),
+        ("tree_small_batch", ctypes.c_int32),
     ]
 
 

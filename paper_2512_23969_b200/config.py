@@ -114,7 +114,7 @@ class TuningConfig:
             kw = {}
             for key in ("fors_trees_per_set", "fors_sets_fused", "fors_relax", "wots_from_tree", "chunk", "streams",
                         "shared_layers", "shared_auto", "fors_cta_levels", "tree_split", "overlap",
-                        "fors_small_batch"):
+                        "fors_small_batch", "tree_small_batch"):
                 if key in b:
                     kw[key] = b[key]
             if "variant" in b:
@@ -134,7 +134,7 @@ class TuningConfig:
                 "wots_from_tree": e["wots_from_tree"], "chunk": e["chunk"], "streams": e["streams"],
                 "shared_layers": e["shared_layers"], "shared_auto": e["shared_auto"],
                 "fors_cta_levels": e["fors_cta_levels"], "tree_split": e["tree_split"], "overlap": e["overlap"],
-                "fors_small_batch": e["fors_small_batch"],
+                "fors_small_batch": e["fors_small_batch"], "tree_small_batch": e["tree_small_batch"],
             }
             cfg.sets[set_id].backends = {k: "tuned" if e["variant"][k] else "baseline" for k in KERNELS}
         return cfg

@@ -128,9 +128,10 @@ hs_set_config default_config(int set) {
   c.tree_split = 2;
   // streams for graphs of at most this many messages (1 = always): measured
   // crossover on B200, profiles/r02y_overlap_crossover.txt
-  static const int ov[3] = {1, 1536, 8192}, small[3] = {64, 64, 0};
+  static const int ov[3] = {1, 1536, 8192}, fsmall[3] = {64, 64, 0}, tsmall[3] = {64, 16, 16};
   c.overlap = ov[set];
-  c.fors_small_batch = small[set];
+  c.fors_small_batch = fsmall[set];
+  c.tree_small_batch = tsmall[set];
   return c;
 }
 
@@ -311,7 +312,8 @@ int check_layout(hs_t* h, int set, const hs_set_config& c) {
   if (c.shared_auto != 0 && c.shared_auto != 1) return fail(h, HS_E_CONFIG, "shared_auto must be 0 or 1");
   if (c.tree_split < 0 || c.tree_split > 2) return fail(h, HS_E_CONFIG, "tree_split must be 0, 1 or 2");
   if (c.overlap < 0) return fail(h, HS_E_CONFIG, "overlap must be 0, 1 or a message count >= 2");
-  if (c.fors_small_batch < 0) return fail(h, HS_E_CONFIG, "fors_small_batch must be >= 0");
+  if (c.fors_small_batch < 0 || c.tree_small_batch < 0)
+    return fail(h, HS_E_CONFIG, "fors_small_batch / tree_small_batch must be >= 0");
   if (c.fors_cta_levels < -1 || c.fors_cta_levels > I.log_t)
     return fail(h, HS_E_CONFIG, "fors_cta_levels must be -1 (auto) or in 0..%d", I.log_t);
   return HS_OK;
@@ -361,17 +363,22 @@ int fors_cta_levels(int set, const hs_set_config& c, uint32_t count) {
 
 // The execution shape of one batch graph of `count` messages: the set's
 // config with the batch-size rules resolved.  Small graphs leave most SMs
-// idle, so (a) FORS_Sign runs one tree per CTA (k CTAs per message instead of
-// a few wide ones whose lanes walk several trees in passes) and (b) the FORS /
-// TREE / shared-subtree branches run concurrently; large graphs keep the
-// tuned layout and, where concurrency measured slower (192f, 256f at 16,384),
-// one stream order.  Bytes never depend on the shape.
+// idle and are latency bound, so (a) FORS_Sign runs one tree per CTA (k CTAs
+// per message instead of a few wide ones whose lanes walk several trees in
+// passes), (b) the subtree Merkle levels are warp-shuffle combines (hp H's on
+// the critical path, not leaves-1) and (c) the FORS / TREE / shared-subtree
+// branches run concurrently; large graphs keep the tuned layout, the
+// one-thread-per-subtree Merkle grid and, where concurrency measured slower
+// (192f, 256f at 16,384), one stream order.  Bytes never depend on the shape.
+// Thresholds: profiles/r02x_small_batch_overlap.txt, r02y_overlap_crossover.txt,
+// r02aa_small_batch_tree_shape.txt.
 hs_set_config batch_config(const hs_set_config& c, uint32_t count) {
   hs_set_config b = c;
   if (c.fors_small_batch > 0 && count <= (uint32_t)c.fors_small_batch) {
     b.fors_trees_per_set = 1;
     b.fors_sets_fused = 1;
   }
+  if (c.tree_small_batch > 0 && count <= (uint32_t)c.tree_small_batch && c.tree_split == 2) b.tree_split = 1;
   b.overlap = (c.overlap == 1 || (c.overlap > 1 && count <= (uint32_t)c.overlap)) ? 1 : 0;
   return b;
 }
@@ -516,8 +523,7 @@ int ensure_scratch(hs_t* h, int set, uint32_t count) {
 
 // Issue the signing DAG.  `capture` selects external (graph-visible) timing
 // events; `serial` puts every kernel on s0 back to back.
-cudaError_t enqueue(hs_t* h, int set, const LaunchArgs& a, bool capture, bool serial) {
-  const hs_set_config& c = h->sets[set].cfg;
+cudaError_t enqueue(hs_t* h, int set, const hs_set_config& c, const LaunchArgs& a, bool capture, bool serial) {
   auto rec = [&](int i, cudaStream_t s) {
     return capture ? cudaEventRecordWithFlags(h->ev[i], s, cudaEventRecordExternal) : cudaEventRecord(h->ev[i], s);
   };
@@ -744,7 +750,8 @@ int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nu
   for (int j = 0; j < kMaxStreams; j++) CUDA_TRY(h, cudaStreamWaitEvent(h->s0, h->d2h_done[slot][j], 0));
   if (mode == 1) {  // serialised kernels with per-kernel events (roofline timing): one chunk
     if (count > chunk) return fail(h, HS_E_USAGE, "serialised timing runs at most one chunk (%u messages)", chunk);
-    CUDA_TRY(h, enqueue(h, set, make_args(h, set, batch_config(St.cfg, count), 0, 0, count), false, true));
+    const hs_set_config bc = batch_config(St.cfg, count);
+    CUDA_TRY(h, enqueue(h, set, bc, make_args(h, set, bc, 0, 0, count), false, true));
     CUDA_TRY(h, cudaEventRecord(h->compute_done[slot], h->s0));
     if (fetch_to) CUDA_TRY(h, cudaMemcpyAsync(fetch_to, S.sigs, count * sb, cudaMemcpyDeviceToHost, h->s0));
     if (wsteps_to) CUDA_TRY(h, cudaMemcpyAsync(wsteps_to, S.wsteps, count * 4, cudaMemcpyDeviceToHost, h->s0));
@@ -1299,8 +1306,8 @@ int hs_batch_info(hs_t* h, int set, int32_t* out, int cap) {
     for (uint8_t x : f) built += x != 0;
   }
   const uint32_t graph_count = std::min<uint32_t>(St.staged, (uint32_t)std::max(1, St.cfg.chunk));
-  const int32_t v[5] = {(int32_t)St.staged, St.shared_eff,
-                        fors_cta_levels(set, batch_config(St.cfg, graph_count), graph_count), St.cfg.tree_split, built};
+  const hs_set_config bc = batch_config(St.cfg, graph_count);
+  const int32_t v[5] = {(int32_t)St.staged, St.shared_eff, fors_cta_levels(set, bc, graph_count), bc.tree_split, built};
   const int n = std::min(cap, 5);
   for (int i = 0; i < n; i++) out[i] = v[i];
   return n;
@@ -1405,10 +1412,10 @@ std::string cfg_json(const hs_set_config& c) {
            "{\"fors_trees_per_set\": %d, \"fors_sets_fused\": %d, \"fors_relax\": %d, \"variant\": [%d, %d, %d, %d], "
            "\"use_graph\": %d, \"chunk\": %d, \"wots_from_tree\": %d, \"streams\": %d, \"shared_layers\": %d, "
            "\"shared_auto\": %d, \"fors_cta_levels\": %d, \"tree_split\": %d, \"overlap\": %d, "
-           "\"fors_small_batch\": %d}",
+           "\"fors_small_batch\": %d, \"tree_small_batch\": %d}",
            c.fors_trees_per_set, c.fors_sets_fused, c.fors_relax, c.variant[0], c.variant[1], c.variant[2],
            c.variant[3], c.use_graph, c.chunk, c.wots_from_tree, c.streams, c.shared_layers, c.shared_auto,
-           c.fors_cta_levels, c.tree_split, c.overlap, c.fors_small_batch);
+           c.fors_cta_levels, c.tree_split, c.overlap, c.fors_small_batch, c.tree_small_batch);
   return b;
 }
 
@@ -1554,8 +1561,9 @@ int hs_tune(hs_t* h, int set, uint32_t count, int32_t top, int32_t reps, char* j
   //    of the same messages: (a) when one stream order won at `count`, the
   //    largest of count/2, count/4, ... (>= 16) at which the concurrent
   //    branches are faster becomes the overlap threshold; (b) one FORS tree
-  //    per CTA is kept for graphs up to the largest of 16, 64, 256 messages at
-  //    which it is faster than the tuned layout by more than 2 %.
+  //    per CTA and (c) the warp-shuffle Merkle reduction (tree_split 1 for a
+  //    tree_split 2 config) are each kept for graphs up to the largest of 16,
+  //    64, 256 messages at which they are faster by more than 2 %.
   auto graph_ms = [&](uint32_t n, double& ms) -> int {
     if (int r = hs_config_set(h, set, &c); r != HS_OK) return r;
     if (int r = stage_inputs(h, set, 0, msgs.data(), offs.data(), nullptr, nullptr, 0, n, false); r != HS_OK) return r;
@@ -1565,6 +1573,7 @@ int hs_tune(hs_t* h, int set, uint32_t count, int32_t top, int32_t reps, char* j
     return HS_OK;
   };
   c.fors_small_batch = 0;
+  c.tree_small_batch = 0;
   js += ", \"overlap_ms\": {";
   if (best_ov == 0) {
     bool firstk = true;
@@ -1600,8 +1609,24 @@ int hs_tune(hs_t* h, int set, uint32_t count, int32_t top, int32_t reps, char* j
     if (!(one_tree < tuned * 0.98)) break;
     small = (int)n;
   }
-  js += "}";
+  js += "}, \"tree_small_batch_ms\": {";
   c.fors_small_batch = small;
+  int tsmall = 0;
+  for (uint32_t n : {16u, 64u, 256u}) {
+    if (n > count || c.tree_split != 2) break;
+    double grid, shuffle;
+    c.tree_small_batch = 0;
+    if (int r = graph_ms(n, grid); r != HS_OK) return r;
+    c.tree_small_batch = (int)n;
+    if (int r = graph_ms(n, shuffle); r != HS_OK) return r;
+    char b[96];
+    snprintf(b, sizeof b, "%s\"%u\": [%.4f, %.4f]", n == 16 ? "" : ", ", n, grid, shuffle);
+    js += b;
+    if (!(shuffle < grid * 0.98)) break;
+    tsmall = (int)n;
+  }
+  js += "}";
+  c.tree_small_batch = tsmall;
   c.overlap = small_ov;
   if (int r = stage_inputs(h, set, 0, msgs.data(), offs.data(), nullptr, nullptr, 0, count, false); r != HS_OK)
     return r;

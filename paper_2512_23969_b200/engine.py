@@ -132,6 +132,7 @@ class Engine:
             "tree_split": int(c.tree_split),
             "overlap": int(c.overlap),
             "fors_small_batch": int(c.fors_small_batch),
+            "tree_small_batch": int(c.tree_small_batch),
         }
 
     def set_config(self, set_id: str, **kw) -> dict:
@@ -159,6 +160,7 @@ class Engine:
         c.tree_split = int(cur["tree_split"])
         c.overlap = int(cur["overlap"])
         c.fors_small_batch = int(cur["fors_small_batch"])
+        c.tree_small_batch = int(cur["tree_small_batch"])
         self._check(_lib.lib().hs_config_set(self._h, SET_INDEX[set_id], ctypes.byref(c)), "hs_config_set")
         return self.config(set_id)
 

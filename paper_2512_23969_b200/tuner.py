@@ -277,8 +277,9 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
        concurrent sub-batches, or one stream order) are timed end to end from
        pinned host buffers at ``count`` messages.
     4. The batch-size rules: the overlap threshold below ``count`` (when one
-       stream order won) and the largest graph that runs FORS_Sign with one
-       tree per CTA (``fors_small_batch``), from graph device times.
+       stream order won), the largest graph that runs FORS_Sign with one tree
+       per CTA (``fors_small_batch``) and the largest that reduces subtrees
+       with warp shuffles (``tree_small_batch``), from graph device times.
     Returns the chosen config plus the timing table; the engine is left
     configured with it.
     """
@@ -357,13 +358,14 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
     best_key = min(stable, key=stable.get)
     best_T = int(str(best_key).split("/")[0])
     best_ov = not str(best_key).endswith("/serial")
-    engine.set_config(set_id, streams=best_T, overlap=best_ov, fors_small_batch=0)
+    engine.set_config(set_id, streams=best_T, overlap=best_ov, fors_small_batch=0, tree_small_batch=0)
     # 4. batch-size rules (the engine's batch_config), graph device time on
     #    smaller batches: (a) when one stream order won at `count`, the largest
     #    of count/2, count/4, ... (>= 16) at which the concurrent branches are
-    #    faster becomes the overlap threshold; (b) one FORS tree per CTA is kept
-    #    for graphs up to the largest of 16, 64, 256 messages at which it beats
-    #    the tuned layout by more than tie_tolerance.
+    #    faster becomes the overlap threshold; (b) one FORS tree per CTA and
+    #    (c) the warp-shuffle Merkle reduction (tree_split 1 for a tree_split 2
+    #    config) are each kept for graphs up to the largest of 16, 64, 256
+    #    messages at which they win by more than tie_tolerance.
     def graph_ms(n: int, **kw) -> float:
         engine.set_config(set_id, **kw)
         _synthetic(engine, set_id, n)
@@ -389,8 +391,18 @@ def tune_on_device(engine, set_id: str, count: int = 2048, top: int = 12, reps: 
             break
         small = n
     engine.set_config(set_id, fors_small_batch=small)
+    tree_table, tsmall = {}, 0
+    for n in (16, 64, 256):
+        if n > count or engine.config(set_id)["tree_split"] != 2:
+            break
+        tree_table[n] = (graph_ms(n, tree_small_batch=0), graph_ms(n, tree_small_batch=n))
+        if not tree_table[n][1] < tree_table[n][0] * (1 - tie_tolerance):
+            break
+        tsmall = n
+    engine.set_config(set_id, tree_small_batch=tsmall)
     _synthetic(engine, set_id, count)
     return {"set": set_id, "count": count, "smem_optin": info["smem_optin"], "layouts": table,
             "best_layout": best, "cta_levels_ms": ltable, "variants": variants, "variant_ms": vtable,
             "streams_ms": stable, "overlap_ms": otable, "small_batch_ms": small_table,
+            "tree_small_batch_ms": tree_table,
             "config": engine.config(set_id)}

@@ -144,7 +144,8 @@ def test_on_device_tree_tuning(eng, oracle_mod, native):
         assert (cfg["fors_trees_per_set"], cfg["fors_sets_fused"], cfg["fors_relax"]) == layout
         # step 4: the batch-size rules were timed (graph device times) and set
         assert "overlap_ms" in rep and "small_batch_ms" in rep
-        assert cfg["fors_small_batch"] in (0, 16, 64, 256) and cfg["overlap"] >= 0
+        assert cfg["fors_small_batch"] in (0, 16, 64, 256) and cfg["tree_small_batch"] in (0, 16, 64, 256)
+        assert cfg["overlap"] >= 0 and "tree_small_batch_ms" in rep
         lanes = layout[0] * (p.fors_t // 2 if layout[2] else p.fors_t)
         assert lanes <= 768 and layout[0] * layout[1] <= p.k
         assert hs.Engine.fors_smem_bytes(set_id, *layout) <= eng.device_info()["smem_optin"]

@@ -105,7 +105,7 @@ def test_layouts_and_variants(eng, oracle_mod, set_id, variant, stash):
             split = (2, 0, 1, 2)[i]
             eng.set_config(set_id, fors_trees_per_set=nt, fors_sets_fused=f, fors_relax=bool(rx), wots_from_tree=stash,
                            variant={k: variant for k in ("FORS_Sign", "TREE_Sign", "WOTS_Sign", "host")},
-                           tree_split=split, fors_small_batch=0)  # run the layout as given
+                           tree_split=split, fors_small_batch=0, tree_small_batch=0)  # run the shape as given
             assert eng.sign_batch(set_id, msgs) == ref, (nt, f, rx, split)
         assert eng.keygen_batch(set_id, [seed])[0] == sk  # keygen root kernel on this path
     finally:
@@ -149,7 +149,8 @@ def test_config_change_rebuilds_graph(eng, oracle_mod):
     try:
         counts = {}
         for split, lc in ((1, -1), (0, p.log_t), (1, -1), (2, -1)):
-            eng.set_config(set_id, tree_split=split, fors_cta_levels=lc, streams=1, shared_layers=0)
+            eng.set_config(set_id, tree_split=split, fors_cta_levels=lc, streams=1, shared_layers=0,
+                           tree_small_batch=0)
             n0 = eng.launch_count
             assert eng.sign_batch(set_id, msgs) == ref, (split, lc)
             counts.setdefault((split, lc), []).append(eng.launch_count - n0)
@@ -321,8 +322,9 @@ def test_api_roundtrip_golden(eng, golden):
 def test_batch_size_rules(eng, oracle_mod, set_id):
     """The batch-size rules of the engine (batch_config): graphs of at most
     fors_small_batch messages run FORS_Sign with one tree per CTA, graphs of
-    at most `overlap` (>= 2) messages run the FORS / TREE / shared branches
-    concurrently, larger ones in one stream order.  Counts on both sides of
+    at most tree_small_batch messages reduce subtrees with warp shuffles
+    (tree_split 1), graphs of at most `overlap` (>= 2) messages run the FORS /
+    TREE / shared branches concurrently, larger ones in one stream order.  Counts on both sides of
     each threshold, with Relax on and off, sign the oracle's bytes."""
     p = derive(set_id)
     rng = random.Random(4242)
@@ -334,8 +336,9 @@ def test_batch_size_rules(eng, oracle_mod, set_id):
     base = eng.config(set_id)
     try:
         for relax in (False, True):
-            for small, ov in ((20, 0), (21, 20), (0, 21), (21, 1), (64, 0)):
-                eng.set_config(set_id, fors_relax=relax, fors_small_batch=small, overlap=ov, streams=1)
+            for small, tsmall, ov in ((20, 0, 0), (21, 21, 20), (0, 20, 21), (21, 64, 1), (64, 0, 0)):
+                eng.set_config(set_id, fors_relax=relax, fors_small_batch=small, tree_small_batch=tsmall, overlap=ov,
+                               streams=1, tree_split=2)
                 for n in (1, 20, 21):
                     assert eng.sign_batch(set_id, msgs[:n], key_idx=kidx[:n]) == ref[:n], (relax, small, ov, n)
     finally:

@@ -128,6 +128,7 @@ def test_shipped_tuned_config_is_loadable_and_in_range():
         assert -1 <= b.get("fors_cta_levels", -1) <= derive(set_id).log_t
         assert b.get("tree_split", 1) in (0, 1, 2)
         assert int(b.get("overlap", 1)) >= 0 and int(b.get("fors_small_batch", 0)) >= 0
+        assert int(b.get("tree_small_batch", 0)) >= 0
 
 
 class _FakeSigner:
