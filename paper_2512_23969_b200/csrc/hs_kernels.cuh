@@ -232,24 +232,48 @@ __global__ void msg_prep_kernel(LaunchArgs a) {
     if (mlen <= kShortMsgBytes) sha_prefix_words<V, 3 * NW>(dig0, 0, pre, mw, mlen);
     else sha_prefix_msg<V, 3 * NW>(dig0, 0, pre, msg, mlen);
   }
-  uint8_t dg[64];
+  // MGF1 counter blocks: SHA-256(R || PK.seed || dig0 || c) for c = 0, 1.
+  // R || PK.seed || dig0[0..] fill the first block for every counter, so it
+  // is compressed once; each counter then costs one block.  The digest stays
+  // in registers as big-endian words (dw), every byte and bit below is read
+  // at a compile-time position.
   constexpr int nctr = (Pr::digest_bytes + 31) / 32;
-#pragma unroll 1
+  constexpr int PW = 2 * NW + 8;  // prefix words before the counter
+  static_assert(PW >= 16 && PW < 16 + 14, "MGF1 seed spans exactly one full block plus the counter block");
+  uint32_t pre[PW];
+#pragma unroll
+  for (int j = 0; j < NW; j++) { pre[j] = R[j]; pre[NW + j] = K.pk_seed[j]; }
+#pragma unroll
+  for (int j = 0; j < 8; j++) pre[2 * NW + j] = dig0[j];
+  uint32_t m1[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) m1[j] = IVc(j);
+  compress_prep<V>(m1, pre);
+  uint32_t dw[8 * nctr];
+#pragma unroll
   for (int c = 0; c < nctr; c++) {
-    uint32_t pre[2 * NW + 9], o[8];
+    uint32_t W[16], o[8];
 #pragma unroll
-    for (int j = 0; j < NW; j++) { pre[j] = R[j]; pre[NW + j] = K.pk_seed[j]; }
+    for (int j = 0; j < 16; j++) W[j] = 0u;
 #pragma unroll
-    for (int j = 0; j < 8; j++) { pre[2 * NW + j] = dig0[j]; o[j] = IVc(j); }
-    pre[2 * NW + 8] = (uint32_t)c;
-    sha_prefix_msg<V, 2 * NW + 9>(o, 0, pre, msg, 0);
-    for (int j = 0; j < 32; j++) dg[32 * c + j] = (uint8_t)(o[j >> 2] >> (24 - 8 * (j & 3)));
+    for (int j = 16; j < PW; j++) W[j - 16] = pre[j];
+    W[PW - 16] = (uint32_t)c;
+    W[PW - 15] = 0x80000000u;
+    W[15] = (uint32_t)((PW + 1) * 32);
+#pragma unroll
+    for (int j = 0; j < 8; j++) o[j] = m1[j];
+    compress_prep<V>(o, W);
+#pragma unroll
+    for (int j = 0; j < 8; j++) dw[8 * c + j] = o[j];
   }
+  auto dbyte = [&](int b) -> uint32_t { return (dw[b >> 2] >> (24 - 8 * (b & 3))) & 0xFFu; };
   uint64_t tree = 0;
-  for (int j = 0; j < Pr::tree_bytes; j++) tree = (tree << 8) | dg[Pr::fors_msg_bytes + j];
+#pragma unroll
+  for (int j = 0; j < Pr::tree_bytes; j++) tree = (tree << 8) | dbyte(Pr::fors_msg_bytes + j);
   if (Pr::tree_bits < 64) tree &= (1ull << (Pr::tree_bits < 64 ? Pr::tree_bits : 63)) - 1ull;
   uint32_t leaf = 0;
-  for (int j = 0; j < Pr::leaf_bytes; j++) leaf = (leaf << 8) | dg[Pr::fors_msg_bytes + Pr::tree_bytes + j];
+#pragma unroll
+  for (int j = 0; j < Pr::leaf_bytes; j++) leaf = (leaf << 8) | dbyte(Pr::fors_msg_bytes + Pr::tree_bytes + j);
   leaf &= (1u << Pr::leaf_bits) - 1u;
   MsgPlan pl;
   pl.tree = tree;
@@ -267,10 +291,14 @@ __global__ void msg_prep_kernel(LaunchArgs a) {
     }
   }
   // FORS indices, LSB-first bit order within each byte (sigcore.py:75-90)
-  int off = 0;
+#pragma unroll
   for (int g = 0; g < Pr::k; g++) {
     uint32_t v = 0;
-    for (int j = 0; j < Pr::log_t; j++, off++) v |= (uint32_t)((dg[off >> 3] >> (off & 7)) & 1) << j;
+#pragma unroll
+    for (int j = 0; j < Pr::log_t; j++) {
+      const int off = g * Pr::log_t + j;
+      v |= ((dbyte(off >> 3) >> (off & 7)) & 1u) << j;
+    }
     a.indices[(size_t)i * Pr::k + g] = (uint16_t)v;
   }
 }
@@ -1455,7 +1483,7 @@ __global__ void __launch_bounds__(kVerifyThreads) verify_thread_kernel(LaunchArg
     for (int j = 0; j < NW; j++) { pre[j] = R[j]; pre[NW + j] = pk_seed[j]; pre[2 * NW + j] = pk_root[j]; }
 #pragma unroll
     for (int j = 0; j < 8; j++) dig0[j] = IVc(j);
-    sha_prefix_msg<V, 3 * NW>(dig0, 0, pre, msg, mlen);
+    sha_prefix_msg<V, 3 * NW, false>(dig0, 0, pre, msg, mlen);
   }
   uint8_t dg[64];
   constexpr int nctr = (Pr::digest_bytes + 31) / 32;
@@ -1467,7 +1495,7 @@ __global__ void __launch_bounds__(kVerifyThreads) verify_thread_kernel(LaunchArg
 #pragma unroll
     for (int j = 0; j < 8; j++) { pre[2 * NW + j] = dig0[j]; o[j] = IVc(j); }
     pre[2 * NW + 8] = (uint32_t)c;
-    sha_prefix_msg<V, 2 * NW + 9>(o, 0, pre, msg, 0);
+    sha_prefix_msg<V, 2 * NW + 9, false>(o, 0, pre, msg, 0);
     for (int j = 0; j < 32; j++) dg[32 * c + j] = (uint8_t)(o[j >> 2] >> (24 - 8 * (j & 3)));
   }
   uint64_t tree = 0;

@@ -313,12 +313,30 @@ __device__ __noinline__ void compress_compact(uint32_t st[8], const uint32_t Win
 // warp runs it in ~3000 cycles against ~4400 for compress_compact, whose
 // round loop and constant-memory K reads sit on the critical path
 // (tools/lat_probe.cu, profiles/r02t_lat_probe.txt).
+// State and block travel by value (registers under the device ABI), so the
+// call does not stage them through local memory.
+struct ShaState {
+  uint32_t w[8];
+};
+struct ShaBlock {
+  uint32_t w[16];
+};
 template <class V>
-__device__ __noinline__ void compress_ool(uint32_t st[8], const uint32_t Win[16]) {
-  uint32_t W[16];
+__device__ __noinline__ ShaState compress_ool_v(ShaState st, ShaBlock W) {
+  compress<V>(st.w, W.w);
+  return st;
+}
+template <class V>
+__device__ __forceinline__ void compress_ool(uint32_t st[8], const uint32_t Win[16]) {
+  ShaState s;
+  ShaBlock b;
 #pragma unroll
-  for (int j = 0; j < 16; j++) W[j] = Win[j];
-  compress<V>(st, W);
+  for (int j = 0; j < 8; j++) s.w[j] = st[j];
+#pragma unroll
+  for (int j = 0; j < 16; j++) b.w[j] = Win[j];
+  s = compress_ool_v<V>(s, b);
+#pragma unroll
+  for (int j = 0; j < 8; j++) st[j] = s.w[j];
 }
 // message preparation / verify prologue compression: HS_PREP_UNROLLED=0
 // restores the compact form
@@ -332,6 +350,14 @@ __device__ __forceinline__ void compress_prep(uint32_t st[8], const uint32_t W[1
 #else
   compress_compact<V>(st, W);
 #endif
+}
+// the many-thread verify prologue keeps the compact loop (its warps share the
+// SM, the short loop body stays in the instruction cache: 0.5-2 % faster
+// verification than the unrolled form, profiles/r02ae_verify_ab.txt)
+template <class V, bool Prep>
+__device__ __forceinline__ void compress_sel(uint32_t st[8], const uint32_t W[16]) {
+  if (Prep) compress_prep<V>(st, W);
+  else compress_compact<V>(st, W);
 }
 
 // Rounds [0, R) only (no schedule expansion needed while R <= 16).
@@ -641,7 +667,7 @@ __device__ __forceinline__ uint32_t msg_word(const uint8_t* m, uint64_t mlen, ui
   return v | (0x80u << (24 - 8 * r));
 }
 
-template <class V, int P>
+template <class V, int P, bool Prep = true>
 __device__ __forceinline__ void sha_prefix_msg(uint32_t st[8], uint64_t absorbed, const uint32_t (&pre)[P > 0 ? P : 1],
                                                const uint8_t* m, uint64_t mlen) {
   const uint64_t data = 4ull * P + mlen;                 // bytes hashed here
@@ -658,7 +684,7 @@ __device__ __forceinline__ void sha_prefix_msg(uint32_t st[8], uint64_t absorbed
       W[j] = k < P ? pre[k < P ? k : 0] : msg_word(m, mlen, (uint64_t)(k - P));
     }
     if ((uint64_t)b == nblk - 1) { W[14] = (uint32_t)(bits >> 32); W[15] = (uint32_t)bits; }
-    compress_prep<V>(st, W);
+    compress_sel<V, Prep>(st, W);
   }
 #pragma unroll 1
   for (uint64_t b = PB; b < nblk; b++) {
@@ -666,7 +692,7 @@ __device__ __forceinline__ void sha_prefix_msg(uint32_t st[8], uint64_t absorbed
 #pragma unroll
     for (int j = 0; j < 16; j++) W[j] = msg_word(m, mlen, 16 * b + j - P);
     if (b == nblk - 1) { W[14] = (uint32_t)(bits >> 32); W[15] = (uint32_t)bits; }
-    compress_prep<V>(st, W);
+    compress_sel<V, Prep>(st, W);
   }
 }
 
@@ -680,7 +706,7 @@ __device__ __forceinline__ void load_short_msg(const uint8_t* m, uint64_t mlen, 
   for (int j = 0; j < 17; j++) mw[j] = msg_word(m, mlen, (uint64_t)j);
 }
 
-template <class V, int P>
+template <class V, int P, bool Prep = true>
 __device__ __forceinline__ void sha_prefix_words(uint32_t st[8], uint64_t absorbed, const uint32_t (&pre)[P],
                                                  const uint32_t (&mw)[17], uint64_t mlen) {
   const uint64_t data = 4ull * P + mlen;
@@ -697,7 +723,7 @@ __device__ __forceinline__ void sha_prefix_words(uint32_t st[8], uint64_t absorb
       W[j] = k < P ? pre[k < P ? k : 0] : (k - P < 17 ? mw[k - P < 17 ? k - P : 0] : 0u);
     }
     if ((uint32_t)b == nblk - 1) { W[14] = (uint32_t)(bits >> 32); W[15] = (uint32_t)bits; }
-    compress_prep<V>(st, W);
+    compress_sel<V, Prep>(st, W);
   }
 }
 
