@@ -243,6 +243,10 @@ struct hs_ctx {
   // per io slot: its inputs landed (cs), the batch reading them finished (s0),
   // sub-batch j's signatures copied out (ls[j])
   cudaEvent_t h2d_done[kSlots] = {}, compute_done[kSlots] = {}, d2h_done[kSlots][kMaxStreams] = {};
+  // copy-out streams whose d2h_done[slot][j] was recorded since s0 last waited on
+  // that slot's copies (only those are waited on: a 1-message call does not pay
+  // for kMaxStreams event waits and stream syncs)
+  int slot_T[kSlots] = {};
   cudaEvent_t done[kMaxStreams] = {}, joins[kMaxStreams] = {}, fjoin[kMaxStreams] = {}, sh_done = nullptr;
   int last_T = 1;
   // host-side cost of each cudaGraphLaunch since the last hs_launch_stats reset
@@ -747,7 +751,8 @@ int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nu
   if (int rc = ensure_scratch(h, set, chunk); rc != HS_OK) return rc;
   // inputs of this slot landed; earlier copies out of this slot's signatures finished
   CUDA_TRY(h, cudaStreamWaitEvent(h->s0, h->h2d_done[slot], 0));
-  for (int j = 0; j < kMaxStreams; j++) CUDA_TRY(h, cudaStreamWaitEvent(h->s0, h->d2h_done[slot][j], 0));
+  for (int j = 0; j < h->slot_T[slot]; j++) CUDA_TRY(h, cudaStreamWaitEvent(h->s0, h->d2h_done[slot][j], 0));
+  h->slot_T[slot] = 0;
   if (mode == 1) {  // serialised kernels with per-kernel events (roofline timing): one chunk
     if (count > chunk) return fail(h, HS_E_USAGE, "serialised timing runs at most one chunk (%u messages)", chunk);
     const hs_set_config bc = batch_config(St.cfg, count);
@@ -780,6 +785,7 @@ int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nu
           CUDA_TRY(h, cudaMemcpyAsync(wsteps_to + first, S.wsteps + first, (size_t)n * 4, cudaMemcpyDeviceToHost,
                                       h->ls[j]));
         CUDA_TRY(h, cudaEventRecord(h->d2h_done[slot][j], h->ls[j]));
+        h->slot_T[slot] = std::max(h->slot_T[slot], j + 1);
       }
     }
   }
@@ -1168,7 +1174,7 @@ int hs_sign_batch_ex(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs
     if (wots_steps && !wdirect) std::memcpy(wots_steps + pc.first, S.h_wsteps, (size_t)pc.cn * 4);
     return HS_OK;
   };
-  int rc = HS_OK;
+  int rc = HS_OK, Tused = 0;
   uint32_t c = 0;
   for (uint32_t first = 0; first < count && rc == HS_OK; first += chunk, c++) {
     const uint32_t cn = std::min(chunk, count - first);
@@ -1183,13 +1189,16 @@ int hs_sign_batch_ex(hs_t* h, int set, const uint8_t* msgs, const uint64_t* offs
     rc = run_batch(h, set, cn, 0, direct ? sigs + first * sb : S.h_sigs,
                    wots_steps ? (wdirect ? wots_steps + first : S.h_wsteps) : nullptr, &T);
     if (rc) break;
+    Tused = std::max(Tused, T);
     if (int r2 = drain(prev); r2 != HS_OK) return r2;
     prev = Pending{slot, T, first, cn};
   }
   if (rc == HS_OK) rc = drain(prev);
   cudaError_t e = cudaStreamSynchronize(h->s0);
   if (rc == HS_OK && e != cudaSuccess) rc = fail(h, HS_E_CUDA, "sign: %s", cudaGetErrorString(e));
-  for (int j = 0; j < kMaxStreams; j++) {
+  // drain() waited for every copy this call issued; an error path may leave
+  // copies on any copy-out stream
+  for (int j = 0; j < (rc == HS_OK ? Tused : kMaxStreams); j++) {
     e = cudaStreamSynchronize(h->ls[j]);
     if (rc == HS_OK && e != cudaSuccess) rc = fail(h, HS_E_CUDA, "sign copy-out: %s", cudaGetErrorString(e));
   }

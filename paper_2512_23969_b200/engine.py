@@ -28,16 +28,18 @@ def variants() -> tuple[str, ...]:
 
 
 def _u8ptr(buf):
+    """Address (int) of a host buffer for a c_void_p argument, or None.  The
+    caller keeps `buf` alive across the C call."""
     if buf is None:
         return None
-    if isinstance(buf, (bytes,)):
-        return ctypes.cast(ctypes.c_char_p(buf), ctypes.c_void_p)
-    if isinstance(buf, np.ndarray):
-        return ctypes.c_void_p(buf.ctypes.data)
-    if isinstance(buf, (bytearray, memoryview)):
-        return ctypes.cast((ctypes.c_char * len(buf)).from_buffer(buf), ctypes.c_void_p)
     if isinstance(buf, int):
-        return ctypes.c_void_p(buf)
+        return buf
+    if isinstance(buf, np.ndarray):
+        return buf.ctypes.data
+    if isinstance(buf, bytes):
+        return ctypes.cast(ctypes.c_char_p(buf), ctypes.c_void_p).value
+    if isinstance(buf, (bytearray, memoryview)):
+        return ctypes.addressof((ctypes.c_char * len(buf)).from_buffer(buf))
     raise UsageError(f"unsupported buffer type {type(buf).__name__}")
 
 
@@ -424,7 +426,7 @@ class PinnedBuffer:
 def _addr(buf) -> int:
     """Address of a host buffer (bytes / bytearray / numpy array / raw pointer)."""
     ptr = _u8ptr(buf)
-    return int(ptr.value or 0) if ptr is not None else 0
+    return int(ptr or 0)
 
 
 def shard_ranges(count: int, parts: int) -> list[tuple[int, int]]:

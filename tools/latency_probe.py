@@ -50,11 +50,24 @@ def main():
                 t0 = time.perf_counter()
                 eng.sign_into(set_id, h_blob.ptr, offs, count, h_out.ptr)
                 wall.append(time.perf_counter() - t0)
+            # the same C call without the Python wrapper's argument handling
+            from paper_2512_23969_b200 import _lib
+            from paper_2512_23969_b200.engine import SET_INDEX
+            L = _lib.lib()
+            o64 = np.ascontiguousarray(offs, dtype=np.uint64)
+            op, bp, sp = o64.ctypes.data, h_blob.ptr, h_out.ptr
+            raw = []
+            for _ in range(a.reps):
+                t0 = time.perf_counter()
+                rc = L.hs_sign_batch_ex(eng._h, SET_INDEX[set_id], bp, op, None, None, count, sp, None)
+                raw.append(time.perf_counter() - t0)
+                assert rc == 0
             info = eng.batch_info(set_id)
             print(json.dumps({"set": set_id, "count": count,
                               "device_graph_us": round(1e3 * statistics.median(dev), 1),
                               "api_wall_us": round(1e6 * statistics.median(wall), 1),
                               "api_wall_min_us": round(1e6 * min(wall), 1),
+                              "c_call_us": round(1e6 * statistics.median(raw), 1),
                               "batch": info}), flush=True)
             h_blob.free()
             h_out.free()
