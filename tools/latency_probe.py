@@ -46,10 +46,12 @@ def main():
             for _ in range(5):
                 eng.sign_into(set_id, h_blob.ptr, offs, count, h_out.ptr)
             wall = []
+            eng.launch_stats(reset=True)
             for _ in range(a.reps):
                 t0 = time.perf_counter()
                 eng.sign_into(set_id, h_blob.ptr, offs, count, h_out.ptr)
                 wall.append(time.perf_counter() - t0)
+            gl = eng.launch_stats(reset=True)
             # the same C call without the Python wrapper's argument handling
             from paper_2512_23969_b200 import _lib
             from paper_2512_23969_b200.engine import SET_INDEX
@@ -68,6 +70,7 @@ def main():
                               "api_wall_us": round(1e6 * statistics.median(wall), 1),
                               "api_wall_min_us": round(1e6 * min(wall), 1),
                               "c_call_us": round(1e6 * statistics.median(raw), 1),
+                              "host_graph_launch_us": round(gl["mean_us"], 1),
                               "batch": info}), flush=True)
             h_blob.free()
             h_out.free()
