@@ -91,6 +91,10 @@ class TuningConfig:
                 for k, v in b.get("variant", {}).items():
                     if k not in KERNELS + ("host",) or not (isinstance(v, int) and 0 <= v < MAX_VARIANTS):
                         raise ConfigError(f"{set_id}: bad variant {k}={v}")
+                # batch-size rules: message-count thresholds (overlap also 0 / 1 / true / false)
+                for k in ("overlap", "fors_small_batch", "tree_small_batch"):
+                    if k in b and not (isinstance(b[k], int) and int(b[k]) >= 0):
+                        raise ConfigError(f"{set_id}: {k} must be a message count >= 0, got {b[k]!r}")
 
     # -- engine binding --------------------------------------------------
     def apply(self, engine) -> None:

@@ -217,3 +217,16 @@ def test_graph_signer_under_reference_scheduler(oracle_mod):
     ref_sigs, _ = ref_bg.execute_graphs(ref_bg.build_graphs(msgs, 4, 3), 4, ref_signer)
     assert ref_sigs == sigs
     assert signer.compressions == ref_signer.compressions
+
+
+def test_batch_size_rule_fields_validated(tmp_path):
+    """The b200 row's batch-size thresholds (overlap, fors_small_batch,
+    tree_small_batch) must be non-negative message counts."""
+    path = Path(__file__).resolve().parent.parent / "paper_2512_23969_b200" / "b200_tuned.json"
+    cfg = TuningConfig.load(path)
+    assert cfg.sets["192f"].b200["overlap"] >= 2  # a threshold, not a flag
+    for key, bad in (("overlap", -1), ("fors_small_batch", "64"), ("tree_small_batch", -16)):
+        data = cfg.to_dict()
+        data["sets"]["128f"]["b200"][key] = bad
+        with pytest.raises(ConfigError):
+            TuningConfig.from_dict(data)
