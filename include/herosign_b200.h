@@ -227,7 +227,13 @@ HS_API int hs_launch_stats(hs_t *h, double *out, int cap, int reset);
  *      every split between in-CTA levels and level grids (fors_cta_levels);
  *   2. per kernel, every compiled SHA-256 path; a non-native path replaces
  *      native only when > 2% faster (the reference's tie rule);
- *   3. the sub-batch stream count T, timed end to end (hs_sign_batch_ex).
+ *   3. the sub-batch stream count T and stream overlap, timed end to end
+ *      (hs_sign_batch_ex);
+ *   4. the batch-size rules from graph device times on smaller batches: the
+ *      overlap threshold (when one stream order won at `count`) and the
+ *      largest of 16 / 64 / 256 messages at which one FORS tree per CTA
+ *      (fors_small_batch) and the warp-shuffle Merkle reduction
+ *      (tree_small_batch) win by more than 2%.
  * The handle is left configured with the result; json receives a report
  * (layouts, timings, final hs_set_config).  Returns 0, or the report's size
  * + 1 when cap is too small (truncated; the configuration is applied either
