@@ -1441,8 +1441,12 @@ __device__ __forceinline__ void walk_auth(uint32_t node[8], const uint32_t mid[8
 // lanes (1.8-2.4x slower, profiles/r01f_stress_verify_thread.txt); here each
 // thread walks its own signature and the wots_len chains of a layer as ONE
 // flattened loop of F steps (sum of 15 - digit over the chains, nearly the
-// same count for every thread), pushing each chain end into its T_len stream
-// as the chain completes -- so lanes stay busy and no chain ends are stored.
+// same count for every thread), so lanes stay busy.  Each chain end goes to
+// a thread-local array and T_len runs after the loop, every lane compressing
+// block b at the same time: streaming the ends into T_len as chains completed
+// ran each T_len block inside the divergent chain-completion branch, where
+// the warp executed it ~17x per useful lane-block (ncu: a full compression
+// executed 7.8M times next to the F step's 14.8M, profiles/r02ak_*).
 // ---------------------------------------------------------------------------
 constexpr int kVerifyThreads = 128;
 
@@ -1531,11 +1535,11 @@ __global__ void __launch_bounds__(kVerifyThreads) verify_thread_kernel(LaunchArg
 
   // hypertree: per layer, the wots_len chains as one flattened loop of F steps
   const uint8_t* ht = sig + Pr::off_ht;
+  constexpr int M = Pr::wots_len * NW;
+  uint32_t ends[M];  // this layer's chain ends (thread-local; T_len reads them after the loop)
 #pragma unroll 1
   for (int layer = 0; layer < Pr::d; layer++) {
     const uint8_t* wsig = ht + (size_t)layer * Pr::layer_bytes;
-    TStream<V> ts;
-    ts.begin(mid, make_adrs((uint32_t)layer, tree, ADDR_WOTS_PK, leaf_idx, 0, 0), mycol, kVerifyThreads);
     Adrs wa = make_adrs((uint32_t)layer, tree, ADDR_WOTS, leaf_idx, 0, 0);
     uint32_t x[NW], pre5[8];
     int c = -1;
@@ -1544,7 +1548,10 @@ __global__ void __launch_bounds__(kVerifyThreads) verify_thread_kernel(LaunchArg
     while (true) {
       // finish completed chains (a digit of 15 gives a zero-length chain)
       while (s == (uint32_t)(Pr::w - 1)) {
-        if (c >= 0) ts.template push_node<NW>(x);
+        if (c >= 0) {
+#pragma unroll
+          for (int j = 0; j < NW; j++) ends[c * NW + j] = x[j];
+        }
         if (++c >= Pr::wots_len) break;
         load_node<S>(wsig + c * Pr::n, x);
         s = wots_digit<S>(root, c);
@@ -1572,10 +1579,23 @@ __global__ void __launch_bounds__(kVerifyThreads) verify_thread_kernel(LaunchArg
       for (int j = 0; j < NW; j++) x[j] = st[j];
       s++;
     }
-    ts.finish(22u + (uint32_t)(Pr::wots_len * Pr::n));
+    // T_len over the chain ends, every lane on block b together (wots.py:140-143)
     uint32_t node[8];
+    {
+      constexpr uint32_t total = 22u + (uint32_t)(Pr::wots_len * Pr::n);
+      constexpr uint32_t nblk = (total + 9u + 63u) / 64u;
+      const Adrs pa = make_adrs((uint32_t)layer, tree, ADDR_WOTS_PK, leaf_idx, 0, 0);
+      const uint32_t aw[6] = {pa.w0, pa.w1, pa.w2, pa.w3, pa.w4, pa.h5};
 #pragma unroll
-    for (int j = 0; j < 8; j++) node[j] = ts.st[j];
+      for (int j = 0; j < 8; j++) node[j] = mid[j];
+#pragma unroll 1
+      for (uint32_t b = 0; b < nblk; b++) {
+        uint32_t W[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) W[j] = tlen_word<M>(16u * b + j, aw, ends, (64u + total) * 8u, 16u * nblk - 1u);
+        compress<V>(node, W);
+      }
+    }
     walk_auth<S, V>(node, mid, make_adrs((uint32_t)layer, tree, ADDR_HASHTREE, 0, 0, 0), leaf_idx, 0,
                     wsig + Pr::wots_sig_bytes, Pr::hp);
 #pragma unroll
