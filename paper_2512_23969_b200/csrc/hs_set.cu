@@ -27,8 +27,8 @@ cudaError_t launch_var(int which, int variant, const LaunchArgs& a, cudaStream_t
 
 }  // namespace
 
-// Message preparation, key setup, T_k, the WOTS gather and verification are a
-// vanishing share of the work and use the native SHA-256 path; the
+// Message preparation, key setup, T_k and the WOTS gather are a vanishing
+// share of the work and use the native SHA-256 path (verification: Mx<248>); the
 // compression-heavy kernels come from hs_var.cu, one object per (set, path).
 template <>
 cudaError_t launch_kernel<HS_SET>(int which, int variant, const LaunchArgs& a, cudaStream_t s) {
@@ -50,7 +50,9 @@ cudaError_t launch_kernel<HS_SET>(int which, int variant, const LaunchArgs& a, c
                               s>>>(a);
       return cudaGetLastError();
     case K_VERIFY:
-      verify_thread_kernel<S, Native><<<blocks_for(a.count, kVerifyThreads), kVerifyThreads, 0, s>>>(a);
+      // verification is ~86 % WOTS chain steps: the FMA-offload path of the
+      // chain grids (+4..9 % at 65,536 signatures, profiles/r02aw_verify_ab_mx248.txt)
+      verify_thread_kernel<S, Mx<248>><<<blocks_for(a.count, kVerifyThreads), kVerifyThreads, 0, s>>>(a);
       return cudaGetLastError();
     default:
       break;
