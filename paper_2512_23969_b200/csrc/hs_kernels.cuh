@@ -1448,7 +1448,10 @@ __device__ __forceinline__ void walk_auth(uint32_t node[8], const uint32_t mid[8
 // the warp executed it ~17x per useful lane-block (ncu: a full compression
 // executed 7.8M times next to the F step's 14.8M, profiles/r02ak_*).
 // ---------------------------------------------------------------------------
-constexpr int kVerifyThreads = 128;
+#ifndef HS_VERIFY_THREADS
+#define HS_VERIFY_THREADS 128
+#endif
+constexpr int kVerifyThreads = HS_VERIFY_THREADS;
 
 template <int S, class V>
 __global__ void __launch_bounds__(kVerifyThreads) verify_thread_kernel(LaunchArgs a) {
