@@ -424,6 +424,13 @@ def measure_set(eng, info, set_id: str, count: int, steps: int, warmup: int, ran
             eng.sign_into(set_id, h_blob.ptr, h_offs.array(np.uint64)[: nb + 1], nb, h_out.ptr)
             lat.append(time.perf_counter() - t1)
         small[str(nb)] = round(1e6 * statistics.median(lat), 1)
+    # the same small batches' device time (graph, inputs staged; CUDA events)
+    small_dev = {}
+    for nb in small_batches:
+        nb = min(nb, count)
+        eng.stage(set_id, blob[: int(offs[nb])], offs[: nb + 1], nb)
+        eng.bench_run(set_id, nb, 3, 0)
+        small_dev[str(nb)] = round(1e3 * statistics.median(eng.bench_run(set_id, nb, 10, 0)), 1)
     eng.launch_stats(reset=True)
 
     # ---- correctness spot check of the timed e2e output vs the oracle ----
@@ -450,9 +457,10 @@ def measure_set(eng, info, set_id: str, count: int, steps: int, warmup: int, ran
             "e2e_batch_us": round(1e6 * e2e_s / steps, 1),
             "e2e_graph_launches_per_batch": round(e2e_launch["graph_launches"] / max(1, steps), 3),
             "e2e_small_batch_us": small,
+            "device_small_batch_us": small_dev,
             "note": "host time inside cudaGraphLaunch (one graph per batch of up to `chunk` messages); device "
                     "batch time (CUDA events); public-API wall time per batch incl. H2D/D2H; median wall time of "
-                    "small batches (messages: us)",
+                    "small batches (messages: us) and their device graph time",
         },
         "roofline": {
             "bound": "int-issue",
