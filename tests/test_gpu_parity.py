@@ -198,6 +198,32 @@ def test_verify_exhaustive_corruption_128f(eng, golden):
     assert not any(res)
 
 
+@pytest.mark.parametrize("set_id", ("192f", "256f"))
+def test_verify_every_byte_corrupted_batch(eng, oracle_mod, set_id):
+    """Every byte position of a 192f / 256f signature corrupted once (one bit,
+    a different bit per position), verified as one batch next to the intact
+    signatures of a 64-message mixed batch: only the intact ones pass.
+    Exercises every region's failure path (R, FORS leaves and auth, each
+    layer's WOTS chains and auth) on the thread-local T_len verify kernel."""
+    p = derive(set_id)
+    rng = random.Random(606)
+    sk = oracle_mod.keygen(set_id, rng.randbytes(3 * p.n))
+    msgs = [rng.randbytes(rng.choice([0, 32, 100])) for _ in range(64)]
+    eng.upload_keys(set_id, sk)
+    sigs = eng.sign_batch(set_id, msgs)
+    assert sigs[0] == oracle_mod.sign(set_id, sk, msgs[0])
+    pk = sk[2 * p.n:]
+    bad_msgs, bad_sigs = [], []
+    for pos in range(p.sig_bytes):
+        b = bytearray(sigs[pos % len(sigs)])
+        b[pos] ^= 1 << (pos % 8)
+        bad_msgs.append(msgs[pos % len(sigs)])
+        bad_sigs.append(bytes(b))
+    res = eng.verify_batch(set_id, pk, msgs + bad_msgs, sigs + bad_sigs)
+    assert all(res[:len(msgs)])
+    assert not any(res[len(msgs):]), [i for i, r in enumerate(res[len(msgs):]) if r][:10]
+
+
 def test_errors(eng):
     p = derive("128f")
     with pytest.raises(hs.UsageError):
