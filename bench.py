@@ -470,6 +470,11 @@ def measure_set(eng, info, set_id: str, count: int, steps: int, warmup: int, ran
             "unit": "Gcompressions/s",
             "frac": round(achieved / peak, 4),
             "traffic": traffic,
+            "traffic_gbs": round(traffic / (tree_ms_avg / 1e3) / 1e9, 1) if traffic else None,
+            "traffic_note": "DRAM bytes of the per-message TREE_Sign kernels (profiles/tree_traffic.json, ncu): the "
+                            "signing leaf's 16 chain positions per chain kept for the WOTS gather (the digits are "
+                            "known only once the layer below is signed) and the chain ends written once and read "
+                            "once by the leaf grid -- a few % of HBM bandwidth next to an integer-issue-bound kernel",
             "work_per_launch": f"{chunk} msgs x {p.d - rshared_L} layers x {sub} compressions per subtree "
                                f"(executed; {rshared_L} top layers come from {units} shared subtrees)",
             "kernel_ms": round(tree_ms_avg, 3),
