@@ -528,6 +528,18 @@ __device__ __forceinline__ uint32_t tlen_word(uint32_t k, const uint32_t aw[6], 
   return k == last ? len_bits : 0u;
 }
 
+// tlen_word with the two chain-end words it may need already in registers:
+// lo = e[k - 6], hi = e[k - 5] (either may be a don't-care outside the ends).
+template <int M>
+__device__ __forceinline__ uint32_t tlen_word_raw(uint32_t k, const uint32_t aw[6], uint32_t lo, uint32_t hi,
+                                                  uint32_t len_bits, uint32_t last) {
+  if (k < 5) return k == 0 ? aw[0] : k == 1 ? aw[1] : k == 2 ? aw[2] : k == 3 ? aw[3] : aw[4];
+  if (k == 5) return join16(aw[5], hi);
+  if (k < 5 + M) return join16(lo, hi);
+  if (k == 5 + M) return (lo << 16) | 0x8000u;
+  return k == last ? len_bits : 0u;
+}
+
 template <int S, class V>
 __global__ void __launch_bounds__(kTreeBlock) tree_root_kernel(LaunchArgs a) {
   using Pr = P<S>;
@@ -557,12 +569,28 @@ __global__ void __launch_bounds__(kTreeBlock) tree_root_kernel(LaunchArgs a) {
     const uint32_t* e = a.chain_ends + gid * M;
 #pragma unroll
     for (int j = 0; j < 8; j++) node[j] = K->thash_mid[j];
+    // T_len, the chain-end words of block b+1 loaded into registers while
+    // block b compresses: this grid runs the small graphs (tree_small_batch),
+    // where each leaf thread is alone on the critical path and a load per
+    // block would wait a full L2 round trip (raw[i] = e[16b - 6 + i])
+    uint32_t raw[17];
+#pragma unroll
+    for (int i = 0; i < 17; i++) raw[i] = (i >= 6 && i - 6 < M) ? e[i - 6] : 0u;
 #pragma unroll 1
     for (uint32_t b = 0; b < nblk; b++) {
+      uint32_t nxt[17];
+#pragma unroll
+      for (int i = 0; i < 17; i++) {
+        const int idx = (int)(16u * (b + 1u)) - 6 + i;
+        nxt[i] = (b + 1u < nblk && idx >= 0 && idx < M) ? e[idx] : 0u;
+      }
       uint32_t W[16];
 #pragma unroll
-      for (int j = 0; j < 16; j++) W[j] = tlen_word<M>(16u * b + j, aw, e, (64u + total) * 8u, 16u * nblk - 1u);
+      for (int j = 0; j < 16; j++)
+        W[j] = tlen_word_raw<M>(16u * b + j, aw, raw[j], raw[j + 1], (64u + total) * 8u, 16u * nblk - 1u);
       compress<V>(node, W);
+#pragma unroll
+      for (int i = 0; i < 17; i++) raw[i] = nxt[i];
     }
   }
   uint8_t* auth = a.sigs + (size_t)msg * Pr::sig_bytes + Pr::off_ht + (size_t)layer * Pr::layer_bytes +
