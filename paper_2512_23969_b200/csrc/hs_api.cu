@@ -128,7 +128,7 @@ hs_set_config default_config(int set) {
   c.tree_split = 2;
   // streams for graphs of at most this many messages (1 = always): measured
   // crossover on B200, profiles/r02y_overlap_crossover.txt
-  static const int ov[3] = {1, 1536, 8192}, fsmall[3] = {64, 64, 0}, tsmall[3] = {64, 16, 16};
+  static const int ov[3] = {1, 1536, 8192}, fsmall[3] = {64, 64, 16}, tsmall[3] = {64, 16, 16};
   c.overlap = ov[set];
   c.fors_small_batch = fsmall[set];
   c.tree_small_batch = tsmall[set];
