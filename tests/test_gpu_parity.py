@@ -367,5 +367,7 @@ def test_batch_size_rules(eng, oracle_mod, set_id):
                                streams=1, tree_split=2)
                 for n in (1, 20, 21):
                     assert eng.sign_batch(set_id, msgs[:n], key_idx=kidx[:n]) == ref[:n], (relax, small, ov, n)
+                    # the staged graph took the shape the rule gives for n messages
+                    assert eng.batch_info(set_id)["tree_split"] == (1 if n <= tsmall else 2), (tsmall, n)
     finally:
         eng.set_config(set_id, **base)
