@@ -286,3 +286,29 @@ def test_concurrent_public_calls_different_keys(eng, oracle_mod):
         ref = [oracle_mod.sign(set_id, k.to_bytes(), m) for m in work[t]]
         assert got[t] == ref + ref[:3] + ref, f"thread {t}"
     assert eng.config(set_id) == base
+
+
+@pytest.mark.parametrize("set_id", SETS)
+def test_chunks_with_small_tail_graph(eng, oracle_mod, set_id):
+    """A call whose last chunk is a small graph: the full chunks run the
+    throughput shape (tuned FORS layout, Merkle grid, the set's overlap rule)
+    and the 3-message tail runs the small-graph shape (one FORS tree per CTA
+    where enabled, warp-shuffle Merkle) inside the same pipelined call; every
+    signature equals the oracle's and the step counts are exact."""
+    p = derive(set_id)
+    rng = random.Random(7070 + p.n)
+    sk = oracle_mod.keygen(set_id, rng.randbytes(3 * p.n))
+    count = 2 * 512 + 3
+    msgs = [rng.randbytes(rng.choice([0, 32, 77])) for _ in range(count)]
+    eng.upload_keys(set_id, sk)
+    base = eng.config(set_id)
+    try:
+        eng.set_config(set_id, chunk=512)
+        sigs, steps = eng.sign_batch(set_id, msgs, counts=True)
+    finally:
+        eng.set_config(set_id, **base)
+    ref, comps = oracle_mod.sign_many(set_id, sk, None, msgs)
+    bad = [i for i in range(count) if sigs[i] != ref[i]]
+    assert not bad, bad[:10]
+    fixed = sum(compressions_per_signature(p, len(m), digit_sum=0)["total"] for m in msgs)
+    assert sum(steps) == comps - count * p.k - fixed
