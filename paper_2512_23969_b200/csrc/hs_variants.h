@@ -4,7 +4,7 @@
 // tools/variant_sweep.py choose them from B200 timings of the real kernels).
 #pragma once
 #ifndef HS_MX_MASKS
-#define HS_MX_MASKS 248, 232, 104, 184
+#define HS_MX_MASKS 248, 232, 104, 1272
 #endif
 namespace hs {
 constexpr int kMxMaskList[] = {HS_MX_MASKS};
