@@ -953,6 +953,19 @@ constexpr int kForsMaxLanes = 768;
 #endif
 template <int S>
 constexpr int kForsLaunchBound = S == 0 ? HS_FORS_LB_S0 : S == 1 ? HS_FORS_LB_S1 : HS_FORS_LB_S2;
+// minimum resident CTAs per SM the launch bound asks ptxas for (register cap
+// 65536 / (bound x minB)); 1 = no cap beyond the bound
+#ifndef HS_FORS_MINB_S0
+#define HS_FORS_MINB_S0 1
+#endif
+#ifndef HS_FORS_MINB_S1
+#define HS_FORS_MINB_S1 1
+#endif
+#ifndef HS_FORS_MINB_S2
+#define HS_FORS_MINB_S2 1
+#endif
+template <int S>
+constexpr int kForsMinBlocks = S == 0 ? HS_FORS_MINB_S0 : S == 1 ? HS_FORS_MINB_S1 : HS_FORS_MINB_S2;
 // per-message PRF / F prefix states (16 words) and per-level H prefix states
 // ((log_t + 1) x 8 words, log_t <= 9) at the head of FORS_Sign's smem
 constexpr int kForsPrefixWords = 16 + 8 * 10;
@@ -1016,7 +1029,7 @@ __device__ __forceinline__ void fors_leaf(const uint32_t mid[8], const uint32_t*
 }
 
 template <int S, class V>
-__global__ void __launch_bounds__(kForsLaunchBound<S>) fors_sign_kernel(LaunchArgs a) {
+__global__ void __launch_bounds__(kForsLaunchBound<S>, kForsMinBlocks<S>) fors_sign_kernel(LaunchArgs a) {
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
   constexpr int t = Pr::t;
