@@ -18,6 +18,5 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --l
 python tools/launch_summary.py $OUT/launches_bench_cmd.csv > $OUT/launches_bench_cmd.md 2>&1; head -8 $OUT/launches_bench_cmd.md
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tree_chain -c 1 -o $OUT/tree_chain128f -f python tools/ncu_target.py --set 128f --count 4096 --runs 1 --mode 1 > $OUT/ncu_full.log 2>&1
 timeout 2400 python tools/stress_c5.py > $OUT/stress_c5.txt 2>&1; grep '"set"' $OUT/stress_c5.txt
-for t in memcheck racecheck synccheck initcheck; do
-  timeout 900 compute-sanitizer --tool $t --error-exitcode 9 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$t.txt 2>&1; echo "smoke $t rc=$?"
-done
+# compute-sanitizer is closed on this GPU pool (runs under it left GPUs needing a reset); the last clean
+# memcheck / racecheck / synccheck / initcheck runs are in profiles/sanitizer/ and profiles/r02c_*.
