@@ -575,11 +575,18 @@ cudaError_t enqueue(hs_t* h, int set, const hs_set_config& c, const LaunchArgs& 
 // Messages [first, first + cn) of sub-batch j of T.  The last sub-batch gets
 // a smaller share than the others (weights H, ..., H, 1): only its D2H copy
 // is not hidden under later compute in hs_sign_batch, so it is kept small.
-#ifndef HS_SUB_HEAD_WEIGHT
-#define HS_SUB_HEAD_WEIGHT 4
+// H per set (public call, interleaved A/B, profiles/r02au_ab_subbatch_weight8.txt
+// and r02ch_): 4 for 128f (8 is 2 % slower: 4,096 messages leave the small
+// last sub-batch too few blocks), 8 for 192f / 256f.  HS_SUB_HEAD_WEIGHT
+// overrides every set.
+#ifdef HS_SUB_HEAD_WEIGHT
+constexpr uint64_t kSubHeadWeight[3] = {HS_SUB_HEAD_WEIGHT, HS_SUB_HEAD_WEIGHT, HS_SUB_HEAD_WEIGHT};
+#else
+constexpr uint64_t kSubHeadWeight[3] = {4, 8, 8};
 #endif
-void sub_range(uint32_t count, int T, int j, uint32_t& first, uint32_t& cn) {
+void sub_range(int set, uint32_t count, int T, int j, uint32_t& first, uint32_t& cn) {
 #ifdef HS_EQUAL_SUBBATCH
+  (void)set;
   const uint32_t per = (count + T - 1) / T;
   first = std::min(count, (uint32_t)j * per);
   cn = std::min(per, count - first);
@@ -589,7 +596,7 @@ void sub_range(uint32_t count, int T, int j, uint32_t& first, uint32_t& cn) {
     cn = count;
     return;
   }
-  const uint64_t H = HS_SUB_HEAD_WEIGHT;  // weight of every sub-batch but the last (which has weight 1)
+  const uint64_t H = kSubHeadWeight[set];  // weight of every sub-batch but the last (which has weight 1)
   const uint64_t W = H * ((uint64_t)T - 1ull) + 1ull;
   auto edge = [&](int i) { return (uint32_t)((uint64_t)count * std::min<uint64_t>(H * (uint64_t)i, W) / W); };
   first = edge(j);
@@ -639,7 +646,7 @@ cudaError_t enqueue_batch(hs_t* h, int set, uint32_t io_first, uint32_t count, i
     if (all.shared_layers > 0) TRY(enqueue_shared(set, c, all, q, kernels));
     for (int j = 0; j < T; j++) {
       uint32_t first, cn;
-      sub_range(count, T, j, first, cn);
+      sub_range(set, count, T, j, first, cn);
       if (cn == 0) break;
       const LaunchArgs a = make_args(h, set, c, io_first + first, first, cn);
       TRY(enqueue_fors(set, c, a, q, kernels));
@@ -662,7 +669,7 @@ cudaError_t enqueue_batch(hs_t* h, int set, uint32_t io_first, uint32_t count, i
   }
   for (int j = 0; j < T; j++) {
     uint32_t first, cn;
-    sub_range(count, T, j, first, cn);
+    sub_range(set, count, T, j, first, cn);
     if (cn == 0) break;
     const LaunchArgs a = make_args(h, set, c, io_first + first, first, cn);
     // TREE_j on priority 1+2j, FORS_j just below it: FORS_j's short CTAs fill
@@ -774,7 +781,7 @@ int run_batch(hs_t* h, int set, uint32_t count, int mode, uint8_t* fetch_to = nu
     if (fetch_to || wsteps_to) {
       for (int j = 0; j < T; j++) {
         uint32_t first, n;
-        sub_range(cn, T, j, first, n);
+        sub_range(set, cn, T, j, first, n);
         if (n == 0) break;
         first += c0;
         CUDA_TRY(h, cudaStreamWaitEvent(h->ls[j], h->done[j], 0));
