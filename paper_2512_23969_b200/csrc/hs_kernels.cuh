@@ -966,6 +966,18 @@ constexpr int kForsLaunchBound = S == 0 ? HS_FORS_LB_S0 : S == 1 ? HS_FORS_LB_S1
 #endif
 template <int S>
 constexpr int kForsMinBlocks = S == 0 ? HS_FORS_MINB_S0 : S == 1 ? HS_FORS_MINB_S1 : HS_FORS_MINB_S2;
+// A second, narrow instantiation for layouts of at most kForsNarrowLanes<S>
+// lanes, compiled for kForsNarrowMinB<S> resident CTAs (64 registers): 192f
+// (256 lanes x 4) and 256f (512 x 2) one-tree-per-set layouts run 0.4 / 0.55 %
+// faster than under the 768-lane bound (profiles/r02cc_fors_occupancy_ab.txt).
+// HS_FORS_NARROW=0 builds the wide kernel only.
+#ifndef HS_FORS_NARROW
+#define HS_FORS_NARROW 1
+#endif
+template <int S>
+constexpr int kForsNarrowLanes = !HS_FORS_NARROW ? 0 : S == 1 ? 256 : S == 2 ? 512 : 0;
+template <int S>
+constexpr int kForsNarrowMinB = S == 1 ? 4 : 2;
 // per-message PRF / F prefix states (16 words) and per-level H prefix states
 // ((log_t + 1) x 8 words, log_t <= 9) at the head of FORS_Sign's smem
 constexpr int kForsPrefixWords = 16 + 8 * 10;
@@ -1028,8 +1040,8 @@ __device__ __forceinline__ void fors_leaf(const uint32_t mid[8], const uint32_t*
   compress_resume<V, 5>(leaf_out, sR, W);
 }
 
-template <int S, class V>
-__global__ void __launch_bounds__(kForsLaunchBound<S>, kForsMinBlocks<S>) fors_sign_kernel(LaunchArgs a) {
+template <int S, class V, int LB = kForsLaunchBound<S>, int MINB = kForsMinBlocks<S>>
+__global__ void __launch_bounds__(LB, MINB) fors_sign_kernel(LaunchArgs a) {
   using Pr = P<S>;
   constexpr int NW = Pr::NW;
   constexpr int t = Pr::t;

@@ -33,10 +33,20 @@ cudaError_t launch_variant<HS_SET, HS_VAR>(int which, const LaunchArgs& a, cudaS
       const bool leaves_only = a.fors_cta_levels == (relax ? 1 : 0);
       const size_t smem =
           ((leaves_only ? 0 : (size_t)tpc * fors_smem_words_per_tree<S>(relax)) + kForsPrefixWords) * 4;
+      const unsigned grid = (unsigned)((uint64_t)a.count * passes);
+      if constexpr (kForsNarrowLanes<S> > 0) {
+        if (lanes <= kForsNarrowLanes<S>) {
+          auto* k = fors_sign_kernel<S, V, kForsNarrowLanes<S>, kForsNarrowMinB<S>>;
+          cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          if (e != cudaSuccess) return e;
+          k<<<grid, lanes, smem, s>>>(a);
+          break;
+        }
+      }
       cudaError_t e = cudaFuncSetAttribute(fors_sign_kernel<S, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
       if (e != cudaSuccess) return e;
-      fors_sign_kernel<S, V><<<(unsigned)((uint64_t)a.count * passes), lanes, smem, s>>>(a);
+      fors_sign_kernel<S, V><<<grid, lanes, smem, s>>>(a);
       break;
     }
     case K_FORS_LEVEL:
