@@ -974,10 +974,18 @@ constexpr int kForsMinBlocks = S == 0 ? HS_FORS_MINB_S0 : S == 1 ? HS_FORS_MINB_
 #ifndef HS_FORS_NARROW
 #define HS_FORS_NARROW 1
 #endif
+// 128f's 384-lane layout already fits two CTAs per SM at 80 registers
+// (HS_FORS_NARROW_S0 / HS_FORS_NARROW_MINB_S0 set a narrow bound for it).
+#ifndef HS_FORS_NARROW_S0
+#define HS_FORS_NARROW_S0 0
+#endif
+#ifndef HS_FORS_NARROW_MINB_S0
+#define HS_FORS_NARROW_MINB_S0 3
+#endif
 template <int S>
-constexpr int kForsNarrowLanes = !HS_FORS_NARROW ? 0 : S == 1 ? 256 : S == 2 ? 512 : 0;
+constexpr int kForsNarrowLanes = !HS_FORS_NARROW ? 0 : S == 0 ? HS_FORS_NARROW_S0 : S == 1 ? 256 : 512;
 template <int S>
-constexpr int kForsNarrowMinB = S == 1 ? 4 : 2;
+constexpr int kForsNarrowMinB = S == 0 ? HS_FORS_NARROW_MINB_S0 : S == 1 ? 4 : 2;
 // per-message PRF / F prefix states (16 words) and per-level H prefix states
 // ((log_t + 1) x 8 words, log_t <= 9) at the head of FORS_Sign's smem
 constexpr int kForsPrefixWords = 16 + 8 * 10;
