@@ -95,6 +95,9 @@ def test_layouts_and_variants(eng, oracle_mod, set_id, variant, stash):
     ref = [oracle_mod.sign(set_id, sk, m) for m in msgs]
     eng.upload_keys(set_id, sk)
     base = eng.config(set_id)
+    # (N_tree, F, Relax); for 192f / 256f they cover both FORS_Sign
+    # instantiations: the narrow 64-register kernel (<= 256 / 512 lanes: 192f
+    # (1,1,0), (2,5,1); 256f (1,1,0), (2,2,1), (1,5,1)) and the 768-lane one
     layouts = {"128f": [(1, 1, 0), (11, 3, 0), (2, 5, 1), (16, 2, 1)],
                "192f": [(1, 1, 0), (3, 3, 0), (4, 2, 1), (2, 5, 1)],
                "256f": [(1, 1, 0), (2, 2, 1), (1, 5, 1), (3, 6, 1)]}[set_id]
